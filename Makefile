@@ -1,0 +1,68 @@
+# lagom-b200 build. `make` builds everything in-tree (the .so files travel to
+# the GPU box with the gpurun snapshot; they are git-ignored).
+#
+#   liblagom.so       host C++20 library: the drop-in tuner API (include/lagom/*.hpp)
+#   liblagom_coll.so  sm_100a collective kernels + replay engine behind the C-ABI
+#                     (include/lagom_coll.h); nvcc cross-compiles without a GPU
+#   _lagom_py*.so     pybind11 bindings of the C++ API for tests/bench
+#   build/parity_driver  test driver against the product library
+#
+# The host library is compiled with -ffp-contract=off (no FMA contraction) so
+# its doubles round exactly like the reference build (SURVEY finding 2).
+
+PY        ?= python3
+PKG       := paper_2602_20656_b200
+NVCC      ?= nvcc
+CXX       ?= g++
+NLOHMANN  ?= $(shell $(PY) -c "import os,sys;print(os.path.join(sys.prefix,'lib','python3.12','site-packages','include','cudnn_frontend','thirdparty','nlohmann'))")
+PYBIND    ?= $(shell $(PY) -c "import pybind11;print(pybind11.get_include())")
+PYINC     ?= $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['include'])")
+PYEXT     ?= $(shell $(PY) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))")
+CUDA_HOME ?= /usr/local/cuda
+
+HOST_FLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -Wno-dangling-reference -Iinclude -I$(NLOHMANN)
+HOST_SRCS  := $(wildcard $(PKG)/csrc/lagom/*.cpp)
+HOST_OBJS  := $(patsubst $(PKG)/csrc/lagom/%.cpp,build/host/%.o,$(HOST_SRCS))
+
+CU_ARCH    := -gencode arch=compute_100a,code=sm_100a
+CU_FLAGS   := -std=c++17 -O3 $(CU_ARCH) -lineinfo -Xcompiler -fPIC -Iinclude \
+              --expt-relaxed-constexpr -Xptxas -v
+CU_SRCS    := $(wildcard $(PKG)/csrc/coll/*.cu)
+CU_OBJS    := $(patsubst $(PKG)/csrc/coll/%.cu,build/coll/%.o,$(CU_SRCS))
+
+.PHONY: all host coll py oracle clean
+all: host coll py build/parity_driver
+
+host: $(PKG)/liblagom.so
+
+build/host/%.o: $(PKG)/csrc/lagom/%.cpp $(wildcard include/lagom/*.hpp)
+	@mkdir -p build/host
+	$(CXX) $(HOST_FLAGS) -c $< -o $@
+
+$(PKG)/liblagom.so: $(HOST_OBJS)
+	$(CXX) -shared -o $@ $^
+
+build/parity_driver: tests/cpp/parity_driver.cpp $(PKG)/liblagom.so
+	@mkdir -p build
+	$(CXX) $(HOST_FLAGS) $< -L$(PKG) -llagom -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
+
+coll: $(PKG)/liblagom_coll.so
+
+build/coll/%.o: $(PKG)/csrc/coll/%.cu $(wildcard $(PKG)/csrc/coll/*.cuh) include/lagom_coll.h
+	@mkdir -p build/coll
+	$(NVCC) $(CU_FLAGS) -c $< -o $@ 2> build/coll/$*.ptxas.log || (cat build/coll/$*.ptxas.log; false)
+
+$(PKG)/liblagom_coll.so: $(CU_OBJS)
+	$(NVCC) $(CU_ARCH) -shared -o $@ $^ -lcudart -lcublasLt -lcublas -ldl
+
+py: $(PKG)/_lagom_py$(PYEXT)
+
+$(PKG)/_lagom_py$(PYEXT): $(PKG)/csrc/python/bindings.cpp $(PKG)/liblagom.so $(wildcard include/lagom/*.hpp)
+	$(CXX) $(HOST_FLAGS) -shared -I$(PYBIND) -I$(PYINC) $< -L$(PKG) -llagom \
+	    -Wl,-rpath,'$$ORIGIN' -o $@
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(PKG)/*.so
