@@ -1,0 +1,136 @@
+/* lagom-b200 — C-ABI of the sm_100a collective-kernel family (below the
+ * tuner's ProfileFn seam).
+ *
+ * The reference has no device code: a collective there is the analytic
+ * formula comm_time (reference proj/src/commperf.cpp:112-125) over the
+ * tunable tuple CommConfig (reference proj/include/lagom/model.hpp:58-67).
+ * This header is the boundary that turns that tuple into a real launch:
+ *
+ *   CommConfig.algorithm    -> lagom_coll_args_t.algorithm  (RING | TREE)
+ *   CommConfig.protocol     -> lagom_coll_args_t.protocol   (SIMPLE | LL | LL128)
+ *   CommConfig.transport    -> P2P only (NVLink 5 / NVSwitch peer memory)
+ *   CommConfig.num_channels -> grid size  (one CTA per channel)
+ *   CommConfig.num_threads  -> block size (threads per CTA, 64..640 step 64)
+ *   CommConfig.chunk_size   -> bytes of payload per pipeline step per channel
+ *
+ * Every value the reference tuner can emit (reference tuner.cpp:47-76 with
+ * CommBounds defaults, model.hpp:70-76) is accepted.
+ *
+ * Conventions: plain C, POD structs, no exceptions, no torch types. Every
+ * entry point returns lagom_status_t; lagom::b200 (C++) maps non-zero codes
+ * to lagom::Error (reference error.hpp:9-18). Streams are cudaStream_t passed
+ * as void*. One communicator per process per GPU (real mode), or one
+ * communicator emulating all ranks on one GPU (virtual mode, for testing the
+ * protocols without NVLink). The library owns the peer mappings; the caller
+ * owns streams and buffers.
+ */
+#ifndef LAGOM_COLL_H_
+#define LAGOM_COLL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAGOM_COLL_ABI_VERSION 1
+#define LAGOM_MAX_RANKS 8
+#define LAGOM_MAX_CHANNELS 64
+#define LAGOM_HANDLE_BYTES 64 /* == sizeof(cudaIpcMemHandle_t) */
+
+typedef enum {
+  LAGOM_OK = 0,
+  LAGOM_ERR_INVALID_ARGUMENT = 1, /* -> ErrorCode::InvalidInput        */
+  LAGOM_ERR_INVALID_CONFIG = 2,   /* -> ErrorCode::InvalidWorkload     */
+  LAGOM_ERR_CUDA = 3,             /* -> ErrorCode::IoFailure           */
+  LAGOM_ERR_TIMEOUT = 4,          /* peer never answered: IoFailure     */
+  LAGOM_ERR_NOT_READY = 5,        /* peers not imported yet             */
+  LAGOM_ERR_BROKEN = 6            /* an earlier launch aborted          */
+} lagom_status_t;
+
+/* Enum values equal the reference's enum order (model.hpp:37-40). */
+typedef enum { LAGOM_ALL_REDUCE = 0, LAGOM_ALL_GATHER = 1, LAGOM_REDUCE_SCATTER = 2, LAGOM_ALL_TO_ALL = 3 } lagom_collective_t;
+typedef enum { LAGOM_RING = 0, LAGOM_TREE = 1 } lagom_algorithm_t;
+typedef enum { LAGOM_SIMPLE = 0, LAGOM_LL = 1, LAGOM_LL128 = 2 } lagom_protocol_t;
+typedef enum { LAGOM_F32 = 0, LAGOM_BF16 = 1, LAGOM_F16 = 2, LAGOM_I32 = 3 } lagom_dtype_t;
+typedef enum { LAGOM_SUM = 0, LAGOM_MAX = 1, LAGOM_MIN = 2 } lagom_redop_t;
+
+typedef struct {
+  int max_channels;        /* channels provisioned (<= LAGOM_MAX_CHANNELS); default 32 */
+  int steps;               /* pipeline slots per connection; default 4                 */
+  int64_t max_chunk_bytes; /* largest chunk_size accepted; default 4 MiB                */
+  int64_t timeout_ms;      /* spin-wait watchdog; default 10000                         */
+} lagom_comm_opts_t;
+
+typedef struct {
+  int collective;       /* lagom_collective_t */
+  int algorithm;        /* lagom_algorithm_t (TREE: ALL_REDUCE only) */
+  int protocol;         /* lagom_protocol_t */
+  int num_channels;     /* NC: CTAs */
+  int num_threads;      /* NT: threads per CTA */
+  int64_t chunk_bytes;  /* C */
+  int dtype;            /* lagom_dtype_t */
+  int redop;            /* lagom_redop_t (ignored for ALL_GATHER / ALL_TO_ALL) */
+  /* count semantics (NCCL-compatible):
+   *   ALL_REDUCE     send[count]          -> recv[count]
+   *   ALL_GATHER     send[count]          -> recv[nranks*count]
+   *   REDUCE_SCATTER send[nranks*count]   -> recv[count]
+   *   ALL_TO_ALL     send[nranks*count]   -> recv[nranks*count]            */
+  int64_t count;
+} lagom_coll_args_t;
+
+typedef struct lagom_comm* lagom_comm_t;
+
+/* Library / ABI identity. */
+int lagom_coll_abi_version(void);
+const char* lagom_status_string(int status);
+/* Human-readable detail of the last failure on this thread. */
+const char* lagom_last_error(void);
+
+void lagom_comm_default_opts(lagom_comm_opts_t* opts);
+
+/* Real mode: one rank of an nranks job on `device` (cudaSetDevice'd by the
+ * library). Allocates this rank's symmetric heap (staging slots + flags). */
+int lagom_comm_create(int rank, int nranks, int device, const lagom_comm_opts_t* opts,
+                      lagom_comm_t* out);
+/* Writes this rank's cudaIpcMemHandle (LAGOM_HANDLE_BYTES) into `handle`. */
+int lagom_comm_export_handle(lagom_comm_t comm, void* handle);
+/* `handles` = nranks * LAGOM_HANDLE_BYTES, rank order (own entry ignored).
+ * Maps every peer heap; after this the comm is ready. */
+int lagom_comm_import_handles(lagom_comm_t comm, const void* handles);
+
+/* Virtual mode: all `nranks` ranks live on `device` in this process; one
+ * cooperative launch runs every rank's CTAs (grid = NC x nranks). */
+int lagom_comm_create_virtual(int nranks, int device, const lagom_comm_opts_t* opts,
+                              lagom_comm_t* out);
+
+int lagom_comm_destroy(lagom_comm_t comm);
+int lagom_comm_info(lagom_comm_t comm, int* rank, int* nranks, int* device, int* is_virtual);
+/* Bytes of device memory this rank's heap occupies. */
+int64_t lagom_comm_heap_bytes(lagom_comm_t comm);
+/* LAGOM_OK, or LAGOM_ERR_TIMEOUT/BROKEN if a launched kernel aborted. Call
+ * after synchronizing the stream of the launch. */
+int lagom_comm_check(lagom_comm_t comm);
+
+/* Validates (collective, algorithm, protocol, NC, NT, C) against this comm
+ * without launching. */
+int lagom_coll_validate(lagom_comm_t comm, const lagom_coll_args_t* args);
+
+/* Real mode: enqueue one collective on `stream` (cudaStream_t). */
+int lagom_coll_launch(lagom_comm_t comm, const lagom_coll_args_t* args, const void* sendbuf,
+                      void* recvbuf, void* stream);
+/* Virtual mode: sendbufs/recvbufs hold nranks device pointers, rank order. */
+int lagom_coll_launch_virtual(lagom_comm_t comm, const lagom_coll_args_t* args,
+                              const void* const* sendbufs, void* const* recvbufs, void* stream);
+
+/* Algorithmic and bus bytes of one launch (nccl-tests accounting):
+ * algbw bytes S and busbw factor, so busbw = S / t * factor. */
+int lagom_coll_bytes(const lagom_coll_args_t* args, int nranks, int64_t* alg_bytes,
+                     double* bus_factor);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAGOM_COLL_H_ */

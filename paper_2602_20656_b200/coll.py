@@ -1,0 +1,260 @@
+"""Python binding of the collective C-ABI (include/lagom_coll.h) via ctypes.
+
+Host-side mirror of the tuner's kernel-parameter contract: a launch takes
+exactly the fields of the reference's ``CommConfig``
+(reference proj/include/lagom/model.hpp:58-67 — algorithm, protocol,
+transport, num_channels, num_threads, chunk_size) plus the data description.
+Errors follow the reference's convention (reference error.hpp:9-34): a
+non-zero C status becomes ``LagomError`` carrying the matching ``ErrorCode``
+name and a message.
+
+There is no CPU fallback: importing this module on a machine without the
+built ``liblagom_coll.so`` raises, and every launch goes to the sm_100a
+kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liblagom_coll.so")
+
+ALL_REDUCE, ALL_GATHER, REDUCE_SCATTER, ALL_TO_ALL = 0, 1, 2, 3
+RING, TREE = 0, 1
+SIMPLE, LL, LL128 = 0, 1, 2
+F32, BF16, F16, I32 = 0, 1, 2, 3
+SUM, MAX, MIN = 0, 1, 2
+HANDLE_BYTES = 64
+MAX_RANKS = 8
+
+COLLECTIVES = {"ALL_REDUCE": ALL_REDUCE, "ALL_GATHER": ALL_GATHER,
+               "REDUCE_SCATTER": REDUCE_SCATTER, "ALL_TO_ALL": ALL_TO_ALL}
+ALGORITHMS = {"RING": RING, "TREE": TREE}
+PROTOCOLS = {"SIMPLE": SIMPLE, "LL": LL, "LL128": LL128}
+ELEM_BYTES = {F32: 4, BF16: 2, F16: 2, I32: 4}
+
+# C status -> reference ErrorCode name (error.hpp:9-18)
+_STATUS_TO_CODE = {1: "INVALID_INPUT", 2: "INVALID_WORKLOAD", 3: "IO_FAILURE",
+                   4: "IO_FAILURE", 5: "INVALID_INPUT", 6: "IO_FAILURE"}
+
+
+class LagomError(RuntimeError):
+    """Mirror of lagom::Error: ``code`` is the reference ErrorCode name."""
+
+    def __init__(self, code: str, field: str, message: str, status: int = 0):
+        self.code, self.field, self.status = code, field, status
+        super().__init__(f"[{code}] {field}: {message}" if field else f"[{code}] {message}")
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("max_channels", ctypes.c_int), ("steps", ctypes.c_int),
+                ("max_chunk_bytes", ctypes.c_int64), ("timeout_ms", ctypes.c_int64)]
+
+
+class _Args(ctypes.Structure):
+    _fields_ = [("collective", ctypes.c_int), ("algorithm", ctypes.c_int),
+                ("protocol", ctypes.c_int), ("num_channels", ctypes.c_int),
+                ("num_threads", ctypes.c_int), ("chunk_bytes", ctypes.c_int64),
+                ("dtype", ctypes.c_int), ("redop", ctypes.c_int), ("count", ctypes.c_int64)]
+
+
+EXPORTED_SYMBOLS = (
+    "lagom_coll_abi_version", "lagom_status_string", "lagom_last_error",
+    "lagom_comm_default_opts", "lagom_comm_create", "lagom_comm_export_handle",
+    "lagom_comm_import_handles", "lagom_comm_create_virtual", "lagom_comm_destroy",
+    "lagom_comm_info", "lagom_comm_heap_bytes", "lagom_comm_check", "lagom_coll_validate",
+    "lagom_coll_launch", "lagom_coll_launch_virtual", "lagom_coll_bytes",
+)
+
+_lib = None
+
+
+def library() -> ctypes.CDLL:
+    """Loads liblagom_coll.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `make coll` (or __graft_entry__.build())")
+    lib = ctypes.CDLL(_LIB_PATH)
+    c_int, c_i64, vp = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+    sig = {
+        "lagom_coll_abi_version": (c_int, []),
+        "lagom_status_string": (ctypes.c_char_p, [c_int]),
+        "lagom_last_error": (ctypes.c_char_p, []),
+        "lagom_comm_default_opts": (None, [ctypes.POINTER(_Opts)]),
+        "lagom_comm_create": (c_int, [c_int, c_int, c_int, ctypes.POINTER(_Opts), ctypes.POINTER(vp)]),
+        "lagom_comm_export_handle": (c_int, [vp, ctypes.c_char_p]),
+        "lagom_comm_import_handles": (c_int, [vp, ctypes.c_char_p]),
+        "lagom_comm_create_virtual": (c_int, [c_int, c_int, ctypes.POINTER(_Opts), ctypes.POINTER(vp)]),
+        "lagom_comm_destroy": (c_int, [vp]),
+        "lagom_comm_info": (c_int, [vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int),
+                                    ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+        "lagom_comm_heap_bytes": (c_i64, [vp]),
+        "lagom_comm_check": (c_int, [vp]),
+        "lagom_coll_validate": (c_int, [vp, ctypes.POINTER(_Args)]),
+        "lagom_coll_launch": (c_int, [vp, ctypes.POINTER(_Args), vp, vp, vp]),
+        "lagom_coll_launch_virtual": (c_int, [vp, ctypes.POINTER(_Args), ctypes.POINTER(vp),
+                                              ctypes.POINTER(vp), vp]),
+        "lagom_coll_bytes": (c_int, [ctypes.POINTER(_Args), c_int, ctypes.POINTER(c_i64),
+                                     ctypes.POINTER(ctypes.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype, fn.argtypes = res, args
+    _lib = lib
+    return lib
+
+
+def _check(status: int, field: str = "") -> None:
+    if status != 0:
+        lib = library()
+        detail = lib.lagom_last_error().decode() or lib.lagom_status_string(status).decode()
+        raise LagomError(_STATUS_TO_CODE.get(status, "IO_FAILURE"), field, detail, status)
+
+
+@dataclass(frozen=True)
+class CollConfig:
+    """The reference CommConfig tuple (model.hpp:58-67), as launch parameters."""
+    algorithm: int = RING
+    protocol: int = SIMPLE
+    num_channels: int = 1
+    num_threads: int = 64
+    chunk_size: int = 32 * 1024
+
+    @staticmethod
+    def from_reference(cfg: dict) -> "CollConfig":
+        """From the reference JSON config object (json_io.cpp:147-154)."""
+        if cfg.get("transport", "P2P") != "P2P":
+            raise LagomError("INVALID_INPUT", "config.transport", "only P2P exists on one NVSwitch box")
+        return CollConfig(ALGORITHMS[cfg["algorithm"]], PROTOCOLS[cfg["protocol"]],
+                          int(cfg["num_channels"]), int(cfg["num_threads"]), int(cfg["chunk_size"]))
+
+
+def make_args(collective: int, cfg: CollConfig, dtype: int, count: int, redop: int = SUM) -> _Args:
+    return _Args(collective, cfg.algorithm, cfg.protocol, cfg.num_channels, cfg.num_threads,
+                 cfg.chunk_size, dtype, redop, count)
+
+
+def coll_bytes(collective: int, dtype: int, count: int, nranks: int) -> tuple[int, float]:
+    """(algorithmic bytes S, busbw factor) per nccl-tests accounting."""
+    a = _Args(collective, 0, 0, 1, 64, 1024, dtype, 0, count)
+    s, f = ctypes.c_int64(), ctypes.c_double()
+    _check(library().lagom_coll_bytes(ctypes.byref(a), nranks, ctypes.byref(s), ctypes.byref(f)))
+    return s.value, f.value
+
+
+def default_opts() -> _Opts:
+    o = _Opts()
+    library().lagom_comm_default_opts(ctypes.byref(o))
+    return o
+
+
+class Communicator:
+    """One rank of a real (one process per GPU) communicator.
+
+    Bootstrap: every rank creates its heap, exports a CUDA-IPC handle, the
+    handles are all-gathered by the caller's transport (``torch.distributed``
+    in tests/bench, or the C++ shm bootstrap of the replay engine), and each
+    rank imports its peers' heaps.
+    """
+
+    def __init__(self, rank: int, nranks: int, device: int, *, max_channels: int = 32,
+                 steps: int = 4, max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000):
+        lib = library()
+        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms)
+        h = ctypes.c_void_p()
+        _check(lib.lagom_comm_create(rank, nranks, device, ctypes.byref(opts), ctypes.byref(h)), "comm")
+        self._h, self.rank, self.nranks, self.device = h, rank, nranks, device
+
+    def export_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(HANDLE_BYTES)
+        _check(library().lagom_comm_export_handle(self._h, buf), "comm")
+        return buf.raw
+
+    def import_handles(self, handles: Sequence[bytes]) -> None:
+        blob = b"".join(bytes(x) for x in handles)
+        if len(blob) != HANDLE_BYTES * self.nranks:
+            raise LagomError("INVALID_INPUT", "handles", "expected one 64-byte handle per rank")
+        _check(library().lagom_comm_import_handles(self._h, blob), "comm")
+
+    @classmethod
+    def from_process_group(cls, group=None, device: int | None = None, **kw) -> "Communicator":
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        dev = torch.cuda.current_device() if device is None else device
+        comm = cls(rank, world, dev, **kw)
+        handles = [None] * world
+        dist.all_gather_object(handles, comm.export_handle(), group=group)
+        comm.import_handles(handles)
+        return comm
+
+    @property
+    def heap_bytes(self) -> int:
+        return library().lagom_comm_heap_bytes(self._h)
+
+    def launch(self, collective: int, cfg: CollConfig, dtype: int, count: int, send_ptr: int,
+               recv_ptr: int, stream: int = 0, redop: int = SUM) -> None:
+        a = make_args(collective, cfg, dtype, count, redop)
+        _check(library().lagom_coll_launch(self._h, ctypes.byref(a), ctypes.c_void_p(send_ptr),
+                                           ctypes.c_void_p(recv_ptr), ctypes.c_void_p(stream)), "launch")
+
+    def validate(self, collective: int, cfg: CollConfig, dtype: int = F32, count: int = 1) -> None:
+        a = make_args(collective, cfg, dtype, count)
+        _check(library().lagom_coll_validate(self._h, ctypes.byref(a)), "config")
+
+    def check(self) -> None:
+        _check(library().lagom_comm_check(self._h), "comm")
+
+    def close(self) -> None:
+        if self._h:
+            library().lagom_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class VirtualCommunicator:
+    """All ranks emulated on one GPU: one cooperative launch runs every rank's
+    CTAs against per-rank heaps on the same device (protocol testing without
+    NVLink; the kernels and the memory-ordering code are the same)."""
+
+    def __init__(self, nranks: int, device: int = 0, *, max_channels: int = 32, steps: int = 4,
+                 max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000):
+        lib = library()
+        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms)
+        h = ctypes.c_void_p()
+        _check(lib.lagom_comm_create_virtual(nranks, device, ctypes.byref(opts), ctypes.byref(h)), "comm")
+        self._h, self.nranks, self.device = h, nranks, device
+
+    def launch(self, collective: int, cfg: CollConfig, dtype: int, count: int,
+               send_ptrs: Sequence[int], recv_ptrs: Sequence[int], stream: int = 0,
+               redop: int = SUM) -> None:
+        a = make_args(collective, cfg, dtype, count, redop)
+        arr_t = ctypes.c_void_p * self.nranks
+        s = arr_t(*[ctypes.c_void_p(p) for p in send_ptrs])
+        r = arr_t(*[ctypes.c_void_p(p) for p in recv_ptrs])
+        _check(library().lagom_coll_launch_virtual(self._h, ctypes.byref(a), s, r,
+                                                   ctypes.c_void_p(stream)), "launch")
+
+    def check(self) -> None:
+        _check(library().lagom_comm_check(self._h), "comm")
+
+    def close(self) -> None:
+        if self._h:
+            library().lagom_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,383 @@
+// Host side of the collective C-ABI (include/lagom_coll.h): communicator
+// lifetime, symmetric-heap allocation, CUDA-IPC peer mapping over
+// NVLink/NVSwitch, argument validation and kernel dispatch.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "device.cuh"
+#include "lagom_coll.h"
+
+using lagom_dev::KParams;
+
+struct lagom_comm {
+  int rank = 0;
+  int nranks = 1;
+  int device = 0;
+  bool virt = false;
+  bool ready = false;
+  lagom_comm_opts_t opts{};
+  int64_t slot_bytes = 0;
+  int64_t off_ready = 0, off_freed = 0, off_sstep = 0, off_rstep = 0, off_slots = 0;
+  int64_t heap_bytes = 0;
+  char* heap[LAGOM_MAX_RANKS] = {};  // mapped bases (own + peers / all virtual ranks)
+  bool imported[LAGOM_MAX_RANKS] = {};
+  unsigned int* abort_host = nullptr;
+  unsigned int* abort_dev = nullptr;
+  bool broken = false;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& what) {
+  g_last_error = what;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(LAGOM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LAGOM_CUDA(call)                                  \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+void layout(lagom_comm* c) {
+  const int64_t n = c->nranks, ch = c->opts.max_channels;
+  c->slot_bytes = 2 * c->opts.max_chunk_bytes;  // LL doubles the payload
+  int64_t off = 0;
+  c->off_ready = off;
+  off += ch * n * 128;
+  c->off_freed = off;
+  off += ch * n * 128;
+  c->off_sstep = off;
+  off += ch * n * 8;
+  c->off_rstep = off;
+  off += ch * n * 8;
+  off = (off + 4095) / 4096 * 4096;
+  c->off_slots = off;
+  off += ch * n * c->opts.steps * c->slot_bytes;
+  c->heap_bytes = off;
+}
+
+int check_opts(lagom_comm_opts_t* o) {
+  if (o->max_channels < 1 || o->max_channels > LAGOM_MAX_CHANNELS)
+    return fail(LAGOM_ERR_INVALID_ARGUMENT, "max_channels out of range");
+  if (o->steps < 1 || o->steps > 64) return fail(LAGOM_ERR_INVALID_ARGUMENT, "steps out of range");
+  if (o->max_chunk_bytes < 1024 || o->max_chunk_bytes % 1024 != 0)
+    return fail(LAGOM_ERR_INVALID_ARGUMENT, "max_chunk_bytes must be a positive 1 KiB multiple");
+  if (o->timeout_ms < 1) return fail(LAGOM_ERR_INVALID_ARGUMENT, "timeout_ms must be >= 1");
+  return LAGOM_OK;
+}
+
+int alloc_common(lagom_comm* c) {
+  LAGOM_CUDA(cudaSetDevice(c->device));
+  LAGOM_CUDA(cudaHostAlloc(&c->abort_host, sizeof(unsigned int), cudaHostAllocMapped));
+  *c->abort_host = 0;
+  LAGOM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->abort_dev), c->abort_host, 0));
+  return LAGOM_OK;
+}
+
+int elem_bytes_of(int dtype) {
+  switch (dtype) {
+    case LAGOM_F32: return 4;
+    case LAGOM_BF16: return 2;
+    case LAGOM_F16: return 2;
+    case LAGOM_I32: return 4;
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------ dispatch ----
+// One translation unit per protocol (kernels_simple.cu, kernels_ll.cu,
+// kernels_ll128.cu) so the 114 kernel instantiations compile in parallel.
+}  // namespace
+const void* lagom_pick_simple(int kind, int dtype, int op);
+const void* lagom_pick_ll(int kind, int dtype, int op);
+const void* lagom_pick_ll128(int kind, int dtype, int op);
+namespace {
+
+const void* pick_kernel(const lagom_coll_args_t* a) {
+  using namespace lagom_dev;
+  int kind = -1;
+  switch (a->collective) {
+    case LAGOM_ALL_GATHER: kind = kRingAG; break;
+    case LAGOM_REDUCE_SCATTER: kind = kRingRS; break;
+    case LAGOM_ALL_TO_ALL: kind = kA2A; break;
+    case LAGOM_ALL_REDUCE: kind = a->algorithm == LAGOM_TREE ? kTreeAR : kRingAR; break;
+  }
+  switch (a->protocol) {
+    case LAGOM_SIMPLE: return lagom_pick_simple(kind, a->dtype, a->redop);
+    case LAGOM_LL: return lagom_pick_ll(kind, a->dtype, a->redop);
+    case LAGOM_LL128: return lagom_pick_ll128(kind, a->dtype, a->redop);
+  }
+  return nullptr;
+}
+
+int validate(const lagom_comm* c, const lagom_coll_args_t* a) {
+  if (!c || !a) return fail(LAGOM_ERR_INVALID_ARGUMENT, "null comm or args");
+  if (a->collective < 0 || a->collective > LAGOM_ALL_TO_ALL)
+    return fail(LAGOM_ERR_INVALID_ARGUMENT, "unknown collective");
+  if (a->algorithm != LAGOM_RING && a->algorithm != LAGOM_TREE)
+    return fail(LAGOM_ERR_INVALID_ARGUMENT, "unknown algorithm");
+  if (a->protocol < LAGOM_SIMPLE || a->protocol > LAGOM_LL128)
+    return fail(LAGOM_ERR_INVALID_ARGUMENT, "unknown protocol");
+  if (elem_bytes_of(a->dtype) == 0) return fail(LAGOM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (a->redop < LAGOM_SUM || a->redop > LAGOM_MIN) return fail(LAGOM_ERR_INVALID_ARGUMENT, "unknown redop");
+  if (a->count < 0) return fail(LAGOM_ERR_INVALID_ARGUMENT, "count must be >= 0");
+  if (a->num_channels < 1 || a->num_channels > c->opts.max_channels)
+    return fail(LAGOM_ERR_INVALID_CONFIG, "num_channels must lie in [1, " +
+                                              std::to_string(c->opts.max_channels) + "]");
+  if (a->num_threads < 64 || a->num_threads > 640 || a->num_threads % 64 != 0)
+    return fail(LAGOM_ERR_INVALID_CONFIG, "num_threads must be one of {64, 128, ..., 640}");
+  if (a->chunk_bytes < 1024 || a->chunk_bytes % 1024 != 0 || a->chunk_bytes > c->opts.max_chunk_bytes)
+    return fail(LAGOM_ERR_INVALID_CONFIG, "chunk_size must be a 1 KiB multiple in [1 KiB, " +
+                                              std::to_string(c->opts.max_chunk_bytes) + "]");
+  // Tree is an AllReduce schedule (reference keys TREE/* for any collective;
+  // the other collectives fall back to their ring schedule, as NCCL does).
+  return LAGOM_OK;
+}
+
+KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
+  KParams p{};
+  for (int r = 0; r < c->nranks; ++r) p.heap[r] = c->heap[r];
+  p.rank = c->virt ? -1 : c->rank;
+  p.nranks = c->nranks;
+  p.elem_bytes = elem_bytes_of(a->dtype);
+  p.steps = c->opts.steps;
+  p.count = a->count;
+  p.chunk_bytes = a->chunk_bytes;
+  p.slot_bytes = c->slot_bytes;
+  p.off_ready = c->off_ready;
+  p.off_freed = c->off_freed;
+  p.off_sstep = c->off_sstep;
+  p.off_rstep = c->off_rstep;
+  p.off_slots = c->off_slots;
+  p.abort_flag = c->abort_dev;
+  p.timeout_ns = static_cast<uint64_t>(c->opts.timeout_ms) * 1000000ull;
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lagom_coll_abi_version(void) { return LAGOM_COLL_ABI_VERSION; }
+
+const char* lagom_status_string(int s) {
+  switch (s) {
+    case LAGOM_OK: return "ok";
+    case LAGOM_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case LAGOM_ERR_INVALID_CONFIG: return "invalid config";
+    case LAGOM_ERR_CUDA: return "cuda error";
+    case LAGOM_ERR_TIMEOUT: return "peer timeout";
+    case LAGOM_ERR_NOT_READY: return "peers not imported";
+    case LAGOM_ERR_BROKEN: return "communicator broken by an earlier abort";
+  }
+  return "unknown status";
+}
+
+const char* lagom_last_error(void) { return g_last_error.c_str(); }
+
+void lagom_comm_default_opts(lagom_comm_opts_t* o) {
+  o->max_channels = 32;
+  o->steps = 4;
+  o->max_chunk_bytes = 4 << 20;
+  o->timeout_ms = 10000;
+}
+
+int lagom_comm_create(int rank, int nranks, int device, const lagom_comm_opts_t* opts,
+                      lagom_comm_t* out) {
+  if (!out) return fail(LAGOM_ERR_INVALID_ARGUMENT, "null out");
+  if (nranks < 1 || nranks > LAGOM_MAX_RANKS || rank < 0 || rank >= nranks)
+    return fail(LAGOM_ERR_INVALID_ARGUMENT, "rank/nranks out of range");
+  auto* c = new lagom_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  if (opts) c->opts = *opts; else lagom_comm_default_opts(&c->opts);
+  if (int s = check_opts(&c->opts)) { delete c; return s; }
+  layout(c);
+  if (int s = alloc_common(c)) { delete c; return s; }
+  void* h = nullptr;
+  cudaError_t e = cudaMalloc(&h, static_cast<size_t>(c->heap_bytes));
+  if (e == cudaSuccess) e = cudaMemset(h, 0, static_cast<size_t>(c->heap_bytes));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (h) cudaFree(h);
+    cudaFreeHost(c->abort_host);
+    delete c;
+    return cuda_fail(e, "heap allocation");
+  }
+  c->heap[rank] = static_cast<char*>(h);
+  c->imported[rank] = true;
+  c->ready = nranks == 1;
+  *out = c;
+  return LAGOM_OK;
+}
+
+int lagom_comm_export_handle(lagom_comm_t c, void* handle) {
+  if (!c || !handle || c->virt) return fail(LAGOM_ERR_INVALID_ARGUMENT, "export needs a real-mode comm");
+  LAGOM_CUDA(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  LAGOM_CUDA(cudaIpcGetMemHandle(&h, c->heap[c->rank]));
+  std::memcpy(handle, &h, sizeof h);
+  return LAGOM_OK;
+}
+
+int lagom_comm_import_handles(lagom_comm_t c, const void* handles) {
+  if (!c || !handles || c->virt) return fail(LAGOM_ERR_INVALID_ARGUMENT, "import needs a real-mode comm");
+  LAGOM_CUDA(cudaSetDevice(c->device));
+  const char* base = static_cast<const char*>(handles);
+  for (int r = 0; r < c->nranks; ++r) {
+    if (r == c->rank || c->imported[r]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, base + static_cast<size_t>(r) * LAGOM_HANDLE_BYTES, sizeof h);
+    void* p = nullptr;
+    LAGOM_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->heap[r] = static_cast<char*>(p);
+    c->imported[r] = true;
+  }
+  c->ready = true;
+  return LAGOM_OK;
+}
+
+int lagom_comm_create_virtual(int nranks, int device, const lagom_comm_opts_t* opts,
+                              lagom_comm_t* out) {
+  if (!out) return fail(LAGOM_ERR_INVALID_ARGUMENT, "null out");
+  if (nranks < 1 || nranks > LAGOM_MAX_RANKS) return fail(LAGOM_ERR_INVALID_ARGUMENT, "nranks out of range");
+  auto* c = new lagom_comm();
+  c->rank = 0;
+  c->nranks = nranks;
+  c->device = device;
+  c->virt = true;
+  if (opts) c->opts = *opts; else lagom_comm_default_opts(&c->opts);
+  if (int s = check_opts(&c->opts)) { delete c; return s; }
+  layout(c);
+  if (int s = alloc_common(c)) { delete c; return s; }
+  for (int r = 0; r < nranks; ++r) {
+    void* h = nullptr;
+    cudaError_t e = cudaMalloc(&h, static_cast<size_t>(c->heap_bytes));
+    if (e == cudaSuccess) e = cudaMemset(h, 0, static_cast<size_t>(c->heap_bytes));
+    if (e != cudaSuccess) {
+      lagom_comm_destroy(c);
+      return cuda_fail(e, "virtual heap allocation");
+    }
+    c->heap[r] = static_cast<char*>(h);
+    c->imported[r] = true;
+  }
+  LAGOM_CUDA(cudaDeviceSynchronize());
+  c->ready = true;
+  *out = c;
+  return LAGOM_OK;
+}
+
+int lagom_comm_destroy(lagom_comm_t c) {
+  if (!c) return LAGOM_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->nranks; ++r) {
+    if (!c->heap[r]) continue;
+    if (c->virt || r == c->rank) cudaFree(c->heap[r]);
+    else cudaIpcCloseMemHandle(c->heap[r]);
+  }
+  if (c->abort_host) cudaFreeHost(c->abort_host);
+  delete c;
+  return LAGOM_OK;
+}
+
+int lagom_comm_info(lagom_comm_t c, int* rank, int* nranks, int* device, int* is_virtual) {
+  if (!c) return fail(LAGOM_ERR_INVALID_ARGUMENT, "null comm");
+  if (rank) *rank = c->rank;
+  if (nranks) *nranks = c->nranks;
+  if (device) *device = c->device;
+  if (is_virtual) *is_virtual = c->virt ? 1 : 0;
+  return LAGOM_OK;
+}
+
+int64_t lagom_comm_heap_bytes(lagom_comm_t c) { return c ? c->heap_bytes : -1; }
+
+int lagom_comm_check(lagom_comm_t c) {
+  if (!c) return fail(LAGOM_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->broken) return fail(LAGOM_ERR_BROKEN, "communicator broken by an earlier abort");
+  if (*reinterpret_cast<volatile unsigned int*>(c->abort_host) != 0) {
+    c->broken = true;
+    return fail(LAGOM_ERR_TIMEOUT, "a collective kernel timed out waiting for a peer");
+  }
+  return LAGOM_OK;
+}
+
+int lagom_coll_validate(lagom_comm_t c, const lagom_coll_args_t* a) { return validate(c, a); }
+
+int lagom_coll_launch(lagom_comm_t c, const lagom_coll_args_t* a, const void* sendbuf,
+                      void* recvbuf, void* stream) {
+  if (int s = validate(c, a)) return s;
+  if (c->virt) return fail(LAGOM_ERR_INVALID_ARGUMENT, "virtual comm: use lagom_coll_launch_virtual");
+  if (!c->ready) return fail(LAGOM_ERR_NOT_READY, "peer heaps not imported");
+  if (c->broken || *reinterpret_cast<volatile unsigned int*>(c->abort_host)) {
+    c->broken = true;
+    return fail(LAGOM_ERR_BROKEN, "communicator broken by an earlier abort");
+  }
+  if (a->count == 0) return LAGOM_OK;
+  KParams p = make_params(c, a);
+  p.send[0] = static_cast<const char*>(sendbuf);
+  p.recv[0] = static_cast<char*>(recvbuf);
+  const void* k = pick_kernel(a);
+  if (!k) return fail(LAGOM_ERR_INVALID_ARGUMENT, "no kernel for this combination");
+  void* args[] = {&p};
+  LAGOM_CUDA(cudaLaunchKernel(k, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), args, 0,
+                              static_cast<cudaStream_t>(stream)));
+  return LAGOM_OK;
+}
+
+int lagom_coll_launch_virtual(lagom_comm_t c, const lagom_coll_args_t* a,
+                              const void* const* sendbufs, void* const* recvbufs, void* stream) {
+  if (int s = validate(c, a)) return s;
+  if (!c->virt) return fail(LAGOM_ERR_INVALID_ARGUMENT, "real comm: use lagom_coll_launch");
+  if (c->broken || *reinterpret_cast<volatile unsigned int*>(c->abort_host)) {
+    c->broken = true;
+    return fail(LAGOM_ERR_BROKEN, "communicator broken by an earlier abort");
+  }
+  if (a->count == 0) return LAGOM_OK;
+  KParams p = make_params(c, a);
+  for (int r = 0; r < c->nranks; ++r) {
+    p.send[r] = static_cast<const char*>(sendbufs[r]);
+    p.recv[r] = static_cast<char*>(recvbufs[r]);
+  }
+  const void* k = pick_kernel(a);
+  if (!k) return fail(LAGOM_ERR_INVALID_ARGUMENT, "no kernel for this combination");
+  void* args[] = {&p};
+  // Ranks spin on one another: a cooperative launch guarantees that every
+  // rank's CTAs are co-resident (or fails loudly instead of hanging).
+  LAGOM_CUDA(cudaLaunchCooperativeKernel(k, dim3(a->num_channels, c->nranks, 1),
+                                         dim3(a->num_threads, 1, 1), args, 0,
+                                         static_cast<cudaStream_t>(stream)));
+  return LAGOM_OK;
+}
+
+int lagom_coll_bytes(const lagom_coll_args_t* a, int nranks, int64_t* alg_bytes, double* bus_factor) {
+  if (!a || nranks < 1) return fail(LAGOM_ERR_INVALID_ARGUMENT, "bad arguments");
+  const int64_t e = elem_bytes_of(a->dtype);
+  const double n = nranks;
+  int64_t s = 0;
+  double f = 0;
+  switch (a->collective) {
+    case LAGOM_ALL_REDUCE: s = a->count * e; f = 2.0 * (n - 1) / n; break;
+    case LAGOM_ALL_GATHER:
+    case LAGOM_REDUCE_SCATTER:
+    case LAGOM_ALL_TO_ALL: s = a->count * e * nranks; f = (n - 1) / n; break;
+    default: return fail(LAGOM_ERR_INVALID_ARGUMENT, "unknown collective");
+  }
+  if (alg_bytes) *alg_bytes = s;
+  if (bus_factor) *bus_factor = f;
+  return LAGOM_OK;
+}
+
+}  // extern "C"

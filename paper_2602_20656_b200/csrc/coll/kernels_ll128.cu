@@ -1,0 +1,6 @@
+// LAGOM_LL128 instantiations of the collective-kernel family (see device.cuh).
+#include "dispatch.cuh"
+
+const void* lagom_pick_ll128(int kind, int dtype, int op) {
+  return lagom_dev::pick_proto<LAGOM_LL128>(kind, dtype, op);
+}

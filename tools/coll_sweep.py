@@ -1,0 +1,112 @@
+"""Collective bandwidth sweep: lagom sm_100a kernels vs NCCL (torch.distributed),
+one process per GPU. Run under torchrun:
+
+  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+      tools/coll_sweep.py --sizes 1M,64M,512M --out gpurun_out/sweep.jsonl
+
+Each row: collective, protocol, NC, NT, C, bytes, time (max over ranks, CUDA
+events, median of reps), algbw and busbw (nccl-tests accounting).
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2602_20656_b200 import coll as C  # noqa: E402
+
+
+def parse_size(s):
+    s = s.strip().upper()
+    mul = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}.get(s[-1], 1)
+    return int(float(s[:-1] if s[-1] in "KMG" else s) * mul)
+
+
+def time_it(fn, reps, warm, stream):
+    for _ in range(warm):
+        fn()
+    times = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b) / 1e3)
+    times.sort()
+    t = torch.tensor([times[len(times) // 2]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="1M,16M,128M,1G")
+    ap.add_argument("--colls", default="AR,AG,RS,A2A")
+    ap.add_argument("--configs", default="8:512:2M:0,16:512:1M:0,32:640:1M:0,32:640:4M:0,8:512:64K:1,8:512:64K:2,16:640:512K:2")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--warm", type=int, default=2)
+    ap.add_argument("--nccl", type=int, default=1)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = C.Communicator.from_process_group(device=local)
+    stream = torch.cuda.current_stream()
+    s_ptr = stream.cuda_stream
+    names = {"AR": C.ALL_REDUCE, "AG": C.ALL_GATHER, "RS": C.REDUCE_SCATTER, "A2A": C.ALL_TO_ALL}
+    rows = []
+    for size in [parse_size(s) for s in args.sizes.split(",")]:
+        for cn in args.colls.split(","):
+            coll = names[cn]
+            # size = algorithmic bytes S (nccl-tests): AR buffer; AG/RS/A2A total
+            count = size // 2 if coll == C.ALL_REDUCE else size // 2 // world
+            n_in = count if coll in (C.ALL_REDUCE, C.ALL_GATHER) else count * world
+            n_out = count if coll in (C.ALL_REDUCE, C.REDUCE_SCATTER) else count * world
+            x = torch.randn(n_in, device="cuda", dtype=torch.bfloat16)
+            y = torch.empty(n_out, device="cuda", dtype=torch.bfloat16)
+            s_bytes, fac = C.coll_bytes(coll, C.BF16, count, world)
+            for spec in args.configs.split(","):
+                nc, nt, ch, proto = spec.split(":")
+                cfg = C.CollConfig(C.RING, int(proto), int(nc), int(nt), parse_size(ch))
+                fn = lambda: comm.launch(coll, cfg, C.BF16, count, x.data_ptr(), y.data_ptr(), s_ptr)
+                t = time_it(fn, args.reps, args.warm, stream)
+                comm.check()
+                rows.append(dict(impl="lagom", coll=cn, proto=int(proto), nc=int(nc), nt=int(nt),
+                                 chunk=parse_size(ch), bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
+                                 busbw=s_bytes / t * fac / 1e9))
+                if rank == 0:
+                    print(json.dumps(rows[-1]), flush=True)
+            if args.nccl:
+                if coll == C.ALL_REDUCE:
+                    fn = lambda: dist.all_reduce(y.copy_(x) if False else x)
+                elif coll == C.ALL_GATHER:
+                    fn = lambda: dist.all_gather_into_tensor(y, x)
+                elif coll == C.REDUCE_SCATTER:
+                    fn = lambda: dist.reduce_scatter_tensor(y, x)
+                else:
+                    fn = lambda: dist.all_to_all_single(y, x)
+                t = time_it(fn, args.reps, args.warm, stream)
+                rows.append(dict(impl="nccl", coll=cn, bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
+                                 busbw=s_bytes / t * fac / 1e9))
+                if rank == 0:
+                    print(json.dumps(rows[-1]), flush=True)
+    if rank == 0 and args.out:
+        with open(args.out, "w") as f:
+            for r in rows:
+                f.write(json.dumps(r) + "\n")
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
