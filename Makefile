@@ -30,8 +30,8 @@ CU_FLAGS   := -std=c++17 -O3 $(CU_ARCH) -lineinfo -Xcompiler -fPIC -Iinclude \
 CU_SRCS    := $(wildcard $(PKG)/csrc/coll/*.cu)
 CU_OBJS    := $(patsubst $(PKG)/csrc/coll/%.cu,build/coll/%.o,$(CU_SRCS))
 
-.PHONY: all host coll py oracle clean
-all: host coll py build/parity_driver
+.PHONY: all host coll b200 py oracle clean
+all: host coll b200 py build/parity_driver
 
 host: $(PKG)/liblagom.so
 
@@ -55,10 +55,25 @@ build/coll/%.o: $(PKG)/csrc/coll/%.cu $(wildcard $(PKG)/csrc/coll/*.cuh) include
 $(PKG)/liblagom_coll.so: $(CU_OBJS)
 	$(NVCC) $(CU_ARCH) -shared -o $@ $^ -lcudart -lcublasLt -lcublas -ldl
 
+# B200 layer: replay engine, shm coordinator, NCCL (dlopen) baseline.
+B200_SRCS  := $(wildcard $(PKG)/csrc/b200/*.cpp)
+B200_OBJS  := $(patsubst $(PKG)/csrc/b200/%.cpp,build/b200/%.o,$(B200_SRCS))
+CUDA_INC   := -I$(CUDA_HOME)/include
+CUDA_LIBS  := -L$(CUDA_HOME)/lib64 -lcudart -lcublasLt -ldl -lrt
+
+b200: $(PKG)/liblagom_b200.so
+
+build/b200/%.o: $(PKG)/csrc/b200/%.cpp $(wildcard $(PKG)/csrc/b200/*.hpp) $(wildcard include/lagom/*.hpp) include/lagom_coll.h
+	@mkdir -p build/b200
+	$(CXX) $(HOST_FLAGS) $(CUDA_INC) -c $< -o $@
+
+$(PKG)/liblagom_b200.so: $(B200_OBJS) $(PKG)/liblagom.so $(PKG)/liblagom_coll.so
+	$(CXX) -shared -o $@ $(B200_OBJS) -L$(PKG) -llagom -llagom_coll $(CUDA_LIBS) -Wl,-rpath,'$$ORIGIN'
+
 py: $(PKG)/_lagom_py$(PYEXT)
 
-$(PKG)/_lagom_py$(PYEXT): $(PKG)/csrc/python/bindings.cpp $(PKG)/liblagom.so $(wildcard include/lagom/*.hpp)
-	$(CXX) $(HOST_FLAGS) -shared -I$(PYBIND) -I$(PYINC) $< -L$(PKG) -llagom \
+$(PKG)/_lagom_py$(PYEXT): $(PKG)/csrc/python/bindings.cpp $(PKG)/liblagom.so $(PKG)/liblagom_b200.so $(wildcard include/lagom/*.hpp)
+	$(CXX) $(HOST_FLAGS) $(CUDA_INC) -shared -I$(PYBIND) -I$(PYINC) $< -L$(PKG) -llagom_b200 -llagom \
 	    -Wl,-rpath,'$$ORIGIN' -o $@
 
 oracle:

@@ -1,0 +1,165 @@
+// lagom-b200 — B200 layer under the tuner's ProfileFn seam (new, additive API;
+// no reference counterpart — the reference's profiler is the simulator,
+// reference proj/include/lagom/tuner.hpp:15-20 / simulator.hpp:26-43).
+//
+//   ReplayDag        the iteration DAG to execute: the reference Workload's
+//                    shape (ordered compute stream + serialized comm stream +
+//                    ready_after gates, model.hpp:78-96) with real kernels
+//                    attached — cuBLASLt bf16 GEMMs (victims) and collectives.
+//   Coordinator      host-side rank coordination (broadcast / all-gather /
+//                    max-reduce / barrier). make_shm_coordinator() is the
+//                    native one-box implementation over POSIX shared memory.
+//   ReplayEngine     per rank: owns the streams, events, cuBLASLt plans, the
+//                    collective communicator (include/lagom_coll.h) and an
+//                    NCCL communicator for the NCCL-default baseline.
+//   make_gpu_profiler  the measured twin of make_sim_profiler: rank 0 calls it
+//                    from tune(); every other rank sits in ReplayEngine::serve().
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "lagom/model.hpp"
+#include "lagom/simulator.hpp"
+#include "lagom/tuner.hpp"
+
+namespace lagom::b200 {
+
+// ------------------------------------------------------------------- DAG ---
+struct GemmShape {
+  std::int64_t m = 0, n = 0, k = 0;  // D[m,n] = A[m,k] * B[k,n], bf16 in/out, fp32 accumulate
+  std::int64_t batch = 1;            // > 1: strided-batched (attention cores)
+};
+
+struct ReplayComputeOp {
+  std::string id;
+  std::vector<GemmShape> gemms;  // executed back to back on the compute stream
+};
+
+// Element type codes are lagom_dtype_t (include/lagom_coll.h).
+struct ReplayCommOp {
+  std::string id;
+  Collective collective = Collective::AllReduce;
+  int dtype = 1;             // LAGOM_BF16
+  std::int64_t count = 0;    // per lagom_coll.h count semantics
+  std::optional<std::string> ready_after;
+  CommBounds bounds;
+};
+
+struct ReplayDag {
+  std::string name;
+  std::vector<ReplayComputeOp> compute_ops;
+  std::vector<ReplayCommOp> comm_ops;
+};
+
+// Bytes one comm op's message carries in the model (CommOp.message_bytes):
+// the per-rank buffer the collective moves (AR: the buffer; AG/RS/A2A: the
+// full n-block buffer).
+std::int64_t message_bytes(const ReplayCommOp& op, int nranks);
+// FLOPs of one compute op (2*m*n*k*batch summed).
+double compute_flops(const ReplayComputeOp& op);
+
+// The tuner's view of the DAG. Compute ops get wave-model parameters
+// estimated from their GEMM shapes (the contention profiler refits them).
+Workload to_workload(const ReplayDag& dag, const GpuSpec& gpu, int nranks);
+
+// ------------------------------------------------------------ coordinator --
+class Coordinator {
+ public:
+  virtual ~Coordinator() = default;
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  virtual void barrier() = 0;
+  virtual void broadcast(void* buf, std::size_t bytes, int root) = 0;
+  // out = concat over ranks of `bytes` from each rank (rank order).
+  virtual void allgather(const void* in, std::size_t bytes, void* out) = 0;
+  virtual void allreduce_max(double* values, std::size_t n) = 0;
+};
+
+std::unique_ptr<Coordinator> make_single_coordinator();
+// All ranks pass the same unique `name` (e.g. derived from a job token).
+// Rank 0 creates the segment; the others attach (waiting up to timeout_s).
+std::unique_ptr<Coordinator> make_shm_coordinator(const std::string& name, int rank, int size,
+                                                  double timeout_s = 300.0);
+
+// ---------------------------------------------------------------- engine ---
+struct ReplayOptions {
+  int device = 0;
+  int repeats = 3;           // replays per profile call; medians are reported
+  int warmup = 1;            // unrecorded replays before the measured ones
+  bool enable_nccl = true;   // create an NCCL communicator for the baseline
+  std::int64_t max_chunk_bytes = 4 << 20;
+  int max_channels = 32;
+  std::uint64_t seed = 1234;
+  // End-to-end mode (run_e2e): every replay first copies `e2e_in_bytes` from
+  // pinned host memory into the first GEMM's input operand (the step's
+  // activations) and finally reads `e2e_out_bytes` of the last comm op's
+  // result back to pinned host memory; both copies are inside Z.
+  std::int64_t e2e_in_bytes = 0;
+  std::int64_t e2e_out_bytes = 0;
+};
+
+// One measured replay, max over ranks (median over repeats).
+struct ReplayMeasurement {
+  ProfileResult profile;           // x_j, X = sum x_j, Y = sum y_i, Z
+  std::vector<double> comp_times;  // y_i
+  double wall_us = 0.0;            // host wall time of the profile call
+};
+
+class ReplayEngine {
+ public:
+  ReplayEngine(const ReplayDag& dag, Coordinator& coord, const ReplayOptions& opts);
+  ~ReplayEngine();
+  ReplayEngine(const ReplayEngine&) = delete;
+  ReplayEngine& operator=(const ReplayEngine&) = delete;
+
+  const ReplayDag& dag() const;
+  int rank() const;
+  int nranks() const;
+
+  // Collective-call functions: every rank must call them in the same order.
+  // Lagom kernels with one CommConfig per comm op.
+  ReplayMeasurement run(const std::vector<CommConfig>& configs);
+  // Same, end to end (host->device input and device->host result per replay).
+  ReplayMeasurement run_e2e(const std::vector<CommConfig>& configs);
+  // Same DAG, every comm through NCCL with its default parameters.
+  ReplayMeasurement run_nccl();
+  // Compute stream only (isolated victim times y_i).
+  ReplayMeasurement run_compute_only();
+  // Comm stream only with the given configs (isolated x_j).
+  ReplayMeasurement run_comm_only(const std::vector<CommConfig>& configs);
+
+  // Command protocol for make_gpu_profiler: rank 0 drives, others serve().
+  // Returns when rank 0 calls stop().
+  void serve();
+  void stop();  // rank 0 only
+  ReplayMeasurement remote_run(const std::vector<CommConfig>& configs);      // rank 0 only
+  ReplayMeasurement remote_run_e2e(const std::vector<CommConfig>& configs);  // rank 0 only
+  ReplayMeasurement remote_run_nccl();                                       // rank 0 only
+  ReplayMeasurement remote_run_compute_only();                               // rank 0 only
+  ReplayMeasurement remote_run_comm_only(const std::vector<CommConfig>& c);  // rank 0 only
+
+  // Number of profile calls served and the accumulated GPU time of replays.
+  int calls() const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+// The measured ProfileFn (rank 0): broadcasts the configs, every rank replays
+// the DAG, results are max-reduced over ranks. Measurements are not pure
+// (noise), so `record` (optional) receives every (configs, result) pair — a
+// profile table that replays bit-identically through any tuner.
+ProfileFn make_gpu_profiler(ReplayEngine& engine,
+                            std::vector<std::pair<std::vector<CommConfig>, ProfileResult>>* record = nullptr);
+
+// A ProfileFn that answers from a recorded table (exact config-vector match;
+// throws Error(InvalidInput) on a miss). Used to prove that two tuners make
+// identical picks given the same profile table.
+ProfileFn make_table_profiler(std::vector<std::pair<std::vector<CommConfig>, ProfileResult>> table);
+
+}  // namespace lagom::b200

@@ -129,6 +129,12 @@ int lagom_coll_launch_virtual(lagom_comm_t comm, const lagom_coll_args_t* args,
 int lagom_coll_bytes(const lagom_coll_args_t* args, int nranks, int64_t* alg_bytes,
                      double* bus_factor);
 
+/* Synthetic data: fills `nelems` elements of `dtype` with uniform values in
+ * [-scale, scale) (int32: integers in [-2^20, 2^20)) from a counter-based
+ * hash of (seed, index) — deterministic and identical on every GPU. */
+int lagom_fill_random(void* ptr, int64_t nelems, int dtype, uint64_t seed, float scale,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,580 @@
+// Iteration-replay engine: the measured twin of the reference's simulate()
+// (reference simulator.cpp:32-166). It executes the DAG with the same
+// scheduling contract the model assumes —
+//   * compute ops back to back on one stream (cuBLASLt bf16 GEMMs);
+//   * comm ops strictly in order on a second stream, comm j starting after
+//     comm j-1 and after its ready_after compute op (cudaStreamWaitEvent);
+// — and measures with CUDA events: y_i per compute op, x_j per comm op (from
+// the instant the comm stream reaches it to its end, i.e. the model's
+// start/end), Z = last event - start. Results are max-reduced over ranks and
+// the median over `repeats` replays is reported.
+#include <cublasLt.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+
+#include "lagom/b200.hpp"
+#include "lagom/error.hpp"
+#include "lagom_coll.h"
+#include "nccl_dl.hpp"
+
+namespace lagom::b200 {
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(ErrorCode::IoFailure, "cuda", std::string(what) + ": " + cudaGetErrorString(e));
+}
+void lt_check(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS)
+    throw Error(ErrorCode::IoFailure, "cublasLt", std::string(what) + " failed with status " + std::to_string(s));
+}
+void coll_check(int s, const char* what) {
+  if (s != LAGOM_OK) {
+    const ErrorCode code = s == LAGOM_ERR_INVALID_CONFIG ? ErrorCode::InvalidWorkload
+                           : s == LAGOM_ERR_INVALID_ARGUMENT ? ErrorCode::InvalidInput
+                                                             : ErrorCode::IoFailure;
+    throw Error(code, what, lagom_last_error());
+  }
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(ErrorCode::IoFailure, "nccl", std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+int elem_bytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 : 4; }
+
+int coll_code(Collective c) {
+  switch (c) {
+    case Collective::AllReduce: return LAGOM_ALL_REDUCE;
+    case Collective::AllGather: return LAGOM_ALL_GATHER;
+    case Collective::ReduceScatter: return LAGOM_REDUCE_SCATTER;
+    case Collective::AllToAll: return LAGOM_ALL_TO_ALL;
+  }
+  return LAGOM_ALL_REDUCE;
+}
+
+ncclDataType_t nccl_type(int dtype) {
+  switch (dtype) {
+    case LAGOM_F32: return ncclFloat32;
+    case LAGOM_BF16: return ncclBfloat16;
+    case LAGOM_F16: return ncclFloat16;
+    default: return ncclInt32;
+  }
+}
+
+enum class Mode : int { Lagom = 1, Nccl = 2, ComputeOnly = 3, CommOnly = 4, Stop = 5, LagomE2E = 6 };
+
+struct Gemm {
+  GemmShape shape;
+  cublasLtMatmulDesc_t desc = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, d = nullptr;
+  cublasLtMatmulAlgo_t algo{};
+  void *A = nullptr, *B = nullptr, *D = nullptr;
+};
+
+struct Comm {
+  ReplayCommOp op;
+  int dep = -1;
+  void* send = nullptr;
+  void* recv = nullptr;
+  std::int64_t in_elems = 0, out_elems = 0;
+};
+
+template <typename T>
+T median_of(std::vector<T> v) {
+  std::sort(v.begin(), v.end());
+  return v[v.size() / 2];
+}
+
+// Command broadcast from rank 0 to the serving ranks.
+struct WireConfig {
+  std::int32_t algorithm, protocol, transport, num_channels, num_threads, pad;
+  std::int64_t chunk_size;
+};
+
+}  // namespace
+
+// ------------------------------------------------------------- DAG helpers --
+
+std::int64_t message_bytes(const ReplayCommOp& op, int nranks) {
+  const std::int64_t e = elem_bytes(op.dtype);
+  return op.collective == Collective::AllReduce ? op.count * e : op.count * e * nranks;
+}
+
+double compute_flops(const ReplayComputeOp& op) {
+  double f = 0;
+  for (const GemmShape& g : op.gemms)
+    f += 2.0 * static_cast<double>(g.m) * static_cast<double>(g.n) * static_cast<double>(g.k) *
+         static_cast<double>(g.batch);
+  return f;
+}
+
+Workload to_workload(const ReplayDag& dag, const GpuSpec& gpu, int nranks) {
+  Workload w;
+  w.gpu = gpu;
+  for (const ReplayComputeOp& c : dag.compute_ops) {
+    ComputeOp op;
+    op.id = c.id;
+    // One CTA per 256x128 output tile, one resident CTA per SM (sm_100
+    // cuBLASLt bf16 tiles); D = operand + result bytes per tile; theta =
+    // a tile's FLOPs at 1/148 of the measured dense bf16 rate (~1.43 PF/s
+    // sustained) — starting values the contention profiler refits.
+    std::int64_t tiles = 0;
+    double bytes = 0;
+    for (const GemmShape& g : c.gemms) {
+      tiles += ((g.m + 255) / 256) * ((g.n + 127) / 128) * g.batch;
+      bytes += 2.0 * static_cast<double>(g.batch) *
+               static_cast<double>(g.m * g.k + g.k * g.n + g.m * g.n);
+    }
+    op.total_blocks = std::max<std::int64_t>(1, tiles);
+    op.blocks_per_sm = 1;
+    op.bytes_per_block = static_cast<std::int64_t>(bytes / static_cast<double>(op.total_blocks));
+    const double flops_per_tile = compute_flops(c) / static_cast<double>(op.total_blocks);
+    op.base_wave_time = flops_per_tile / (1.43e15 / 148.0) * 1e6;  // us
+    w.compute_ops.push_back(op);
+  }
+  for (const ReplayCommOp& c : dag.comm_ops) {
+    CommOp op;
+    op.id = c.id;
+    op.collective = c.collective;
+    op.message_bytes = std::max<std::int64_t>(1, message_bytes(c, nranks));
+    op.ready_after = c.ready_after;
+    op.bounds = c.bounds;
+    w.comm_ops.push_back(op);
+  }
+  return w;
+}
+
+// ------------------------------------------------------------------ engine --
+
+struct ReplayEngine::Impl {
+  ReplayDag dag;
+  Coordinator& coord;
+  ReplayOptions opts;
+  int rank = 0, n = 1;
+  cudaStream_t cs = nullptr, ks = nullptr;
+  cublasLtHandle_t lt = nullptr;
+  void* workspace = nullptr;
+  std::size_t workspace_bytes = 64ull << 20;
+  std::vector<std::vector<Gemm>> gemms;  // per compute op
+  std::vector<Comm> comms;
+  lagom_comm_t lcomm = nullptr;
+  ncclComm_t ncomm = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_cend = nullptr, ev_kend = nullptr;
+  std::vector<cudaEvent_t> ev_cb, ev_ce, ev_kb, ev_ke;
+  void* host_in = nullptr;   // pinned
+  void* host_out = nullptr;  // pinned
+  int calls = 0;
+
+  Impl(const ReplayDag& d, Coordinator& c, const ReplayOptions& o) : dag(d), coord(c), opts(o) {
+    rank = coord.rank();
+    n = coord.size();
+    cuda_check(cudaSetDevice(opts.device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking), "stream");
+    lt_check(cublasLtCreate(&lt), "cublasLtCreate");
+    cuda_check(cudaMalloc(&workspace, workspace_bytes), "workspace");
+    build_gemms();
+    build_comms();
+    build_comm_backends();
+    auto mk = [](cudaEvent_t* e) { cuda_check(cudaEventCreate(e), "event"); };
+    mk(&ev_start);
+    mk(&ev_cend);
+    mk(&ev_kend);
+    ev_cb.resize(dag.compute_ops.size());
+    ev_ce.resize(dag.compute_ops.size());
+    ev_kb.resize(dag.comm_ops.size());
+    ev_ke.resize(dag.comm_ops.size());
+    for (auto* v : {&ev_cb, &ev_ce, &ev_kb, &ev_ke})
+      for (auto& e : *v) mk(&e);
+    if (opts.e2e_in_bytes > 0) {
+      if (dag.compute_ops.empty() || gemms[0].empty())
+        throw Error(ErrorCode::InvalidInput, "e2e", "end-to-end mode needs a compute op");
+      const Gemm& g0 = gemms[0][0];
+      const std::int64_t cap = g0.shape.k * g0.shape.m * g0.shape.batch * 2;
+      opts.e2e_in_bytes = std::min(opts.e2e_in_bytes, cap);
+      cuda_check(cudaHostAlloc(&host_in, opts.e2e_in_bytes, cudaHostAllocDefault), "pinned in");
+      // synthetic step input, generated once on the device and parked on the host
+      cuda_check(cudaMemcpy(host_in, g0.A, opts.e2e_in_bytes, cudaMemcpyDeviceToHost), "seed host input");
+    }
+    if (opts.e2e_out_bytes > 0) {
+      if (comms.empty()) throw Error(ErrorCode::InvalidInput, "e2e", "end-to-end mode needs a comm op");
+      const Comm& last = comms.back();
+      opts.e2e_out_bytes = std::min<std::int64_t>(opts.e2e_out_bytes, last.out_elems * elem_bytes(last.op.dtype));
+      cuda_check(cudaHostAlloc(&host_out, opts.e2e_out_bytes, cudaHostAllocDefault), "pinned out");
+    }
+    cuda_check(cudaDeviceSynchronize(), "init sync");
+    coord.barrier();
+  }
+
+  ~Impl() {
+    cudaSetDevice(opts.device);
+    cudaDeviceSynchronize();
+    for (auto& ops : gemms)
+      for (Gemm& g : ops) {
+        if (g.desc) cublasLtMatmulDescDestroy(g.desc);
+        if (g.a) cublasLtMatrixLayoutDestroy(g.a);
+        if (g.b) cublasLtMatrixLayoutDestroy(g.b);
+        if (g.d) cublasLtMatrixLayoutDestroy(g.d);
+        cudaFree(g.A);
+        cudaFree(g.B);
+        cudaFree(g.D);
+      }
+    for (Comm& c : comms) {
+      cudaFree(c.send);
+      cudaFree(c.recv);
+    }
+    if (host_in) cudaFreeHost(host_in);
+    if (host_out) cudaFreeHost(host_out);
+    if (ncomm) nccl().CommDestroy(ncomm);
+    if (lcomm) lagom_comm_destroy(lcomm);
+    for (auto* v : {&ev_cb, &ev_ce, &ev_kb, &ev_ke})
+      for (auto& e : *v) cudaEventDestroy(e);
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_cend);
+    cudaEventDestroy(ev_kend);
+    if (lt) cublasLtDestroy(lt);
+    cudaFree(workspace);
+    cudaStreamDestroy(cs);
+    cudaStreamDestroy(ks);
+  }
+
+  void fill(void* p, std::int64_t elems, int dtype, std::uint64_t salt) {
+    coll_check(lagom_fill_random(p, elems, dtype, opts.seed * 1000003ull + salt + 7919ull * rank, 0.02f, cs),
+               "fill");
+  }
+
+  void build_gemms() {
+    std::uint64_t salt = 1;
+    gemms.resize(dag.compute_ops.size());
+    for (std::size_t i = 0; i < dag.compute_ops.size(); ++i) {
+      for (const GemmShape& s : dag.compute_ops[i].gemms) {
+        Gemm g;
+        g.shape = s;
+        // TN (the fast sm_100 layout): A stored k x m (transposed), B k x n,
+        // D m x n, all column-major bf16; fp32 compute.
+        lt_check(cublasLtMatmulDescCreate(&g.desc, CUBLAS_COMPUTE_32F, CUDA_R_32F), "desc");
+        const cublasOperation_t opA = CUBLAS_OP_T, opB = CUBLAS_OP_N;
+        lt_check(cublasLtMatmulDescSetAttribute(g.desc, CUBLASLT_MATMUL_DESC_TRANSA, &opA, sizeof opA), "transa");
+        lt_check(cublasLtMatmulDescSetAttribute(g.desc, CUBLASLT_MATMUL_DESC_TRANSB, &opB, sizeof opB), "transb");
+        lt_check(cublasLtMatrixLayoutCreate(&g.a, CUDA_R_16BF, s.k, s.m, s.k), "layout a");
+        lt_check(cublasLtMatrixLayoutCreate(&g.b, CUDA_R_16BF, s.k, s.n, s.k), "layout b");
+        lt_check(cublasLtMatrixLayoutCreate(&g.d, CUDA_R_16BF, s.m, s.n, s.m), "layout d");
+        if (s.batch > 1) {
+          const int32_t bc = static_cast<int32_t>(s.batch);
+          const int64_t sa = s.k * s.m, sb = s.k * s.n, sd = s.m * s.n;
+          for (auto [lay, stride] : {std::pair{g.a, sa}, std::pair{g.b, sb}, std::pair{g.d, sd}}) {
+            lt_check(cublasLtMatrixLayoutSetAttribute(lay, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof bc), "batch");
+            lt_check(cublasLtMatrixLayoutSetAttribute(lay, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &stride,
+                                                      sizeof stride),
+                     "stride");
+          }
+        }
+        cublasLtMatmulPreference_t pref;
+        lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
+        lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                                      &workspace_bytes, sizeof workspace_bytes),
+                 "pref ws");
+        cublasLtMatmulHeuristicResult_t res{};
+        int found = 0;
+        lt_check(cublasLtMatmulAlgoGetHeuristic(lt, g.desc, g.a, g.b, g.d, g.d, pref, 1, &res, &found), "heuristic");
+        cublasLtMatmulPreferenceDestroy(pref);
+        if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for GEMM shape");
+        g.algo = res.algo;
+        const std::int64_t na = s.k * s.m * s.batch, nb = s.k * s.n * s.batch, nd = s.m * s.n * s.batch;
+        cuda_check(cudaMalloc(&g.A, na * 2), "gemm A");
+        cuda_check(cudaMalloc(&g.B, nb * 2), "gemm B");
+        cuda_check(cudaMalloc(&g.D, nd * 2), "gemm D");
+        fill(g.A, na, LAGOM_BF16, salt++);
+        fill(g.B, nb, LAGOM_BF16, salt++);
+        gemms[i].push_back(g);
+      }
+    }
+  }
+
+  void build_comms() {
+    std::unordered_map<std::string, int> index;
+    for (std::size_t i = 0; i < dag.compute_ops.size(); ++i) index[dag.compute_ops[i].id] = static_cast<int>(i);
+    std::uint64_t salt = 1ull << 32;
+    for (const ReplayCommOp& op : dag.comm_ops) {
+      Comm c;
+      c.op = op;
+      if (op.ready_after) {
+        auto it = index.find(*op.ready_after);
+        if (it == index.end())
+          throw Error(ErrorCode::InvalidWorkload, op.id + ".ready_after", "names no compute op");
+        c.dep = it->second;
+      }
+      const bool in_full = op.collective == Collective::ReduceScatter || op.collective == Collective::AllToAll;
+      const bool out_full = op.collective == Collective::AllGather || op.collective == Collective::AllToAll;
+      c.in_elems = op.count * (in_full ? n : 1);
+      c.out_elems = op.count * (out_full ? n : 1);
+      const int e = elem_bytes(op.dtype);
+      cuda_check(cudaMalloc(&c.send, std::max<std::int64_t>(16, c.in_elems * e)), "comm send");
+      cuda_check(cudaMalloc(&c.recv, std::max<std::int64_t>(16, c.out_elems * e)), "comm recv");
+      fill(c.send, c.in_elems, op.dtype, salt++);
+      comms.push_back(c);
+    }
+  }
+
+  void build_comm_backends() {
+    lagom_comm_opts_t o;
+    lagom_comm_default_opts(&o);
+    o.max_channels = opts.max_channels;
+    o.max_chunk_bytes = opts.max_chunk_bytes;
+    coll_check(lagom_comm_create(rank, n, opts.device, &o, &lcomm), "lagom_comm_create");
+    if (n > 1) {
+      unsigned char mine[LAGOM_HANDLE_BYTES];
+      coll_check(lagom_comm_export_handle(lcomm, mine), "export");
+      std::vector<unsigned char> all(static_cast<std::size_t>(n) * LAGOM_HANDLE_BYTES);
+      coord.allgather(mine, LAGOM_HANDLE_BYTES, all.data());
+      coll_check(lagom_comm_import_handles(lcomm, all.data()), "import");
+    }
+    if (opts.enable_nccl) {
+      ncclUniqueId id{};
+      if (rank == 0) nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+      coord.broadcast(&id, sizeof id, 0);
+      nccl_check(nccl().CommInitRank(&ncomm, n, id, rank), "ncclCommInitRank");
+    }
+  }
+
+  void launch_gemm(const Gemm& g) {
+    const float alpha = 1.0f, beta = 0.0f;
+    lt_check(cublasLtMatmul(lt, g.desc, &alpha, g.A, g.a, g.B, g.b, &beta, g.D, g.d, g.D, g.d, &g.algo,
+                            workspace, workspace_bytes, cs),
+             "cublasLtMatmul");
+  }
+
+  void launch_comm_lagom(const Comm& c, const CommConfig& cfg) {
+    lagom_coll_args_t a{};
+    a.collective = coll_code(c.op.collective);
+    a.algorithm = cfg.algorithm == Algorithm::Tree ? LAGOM_TREE : LAGOM_RING;
+    a.protocol = static_cast<int>(cfg.protocol);
+    a.num_channels = cfg.num_channels;
+    a.num_threads = cfg.num_threads;
+    a.chunk_bytes = cfg.chunk_size;
+    a.dtype = c.op.dtype;
+    a.redop = LAGOM_SUM;
+    a.count = c.op.count;
+    coll_check(lagom_coll_launch(lcomm, &a, c.send, c.recv, ks), c.op.id.c_str());
+  }
+
+  void launch_comm_nccl(const Comm& c) {
+    const NcclApi& api = nccl();
+    const ncclDataType_t t = nccl_type(c.op.dtype);
+    const std::size_t cnt = static_cast<std::size_t>(c.op.count);
+    switch (c.op.collective) {
+      case Collective::AllReduce:
+        nccl_check(api.AllReduce(c.send, c.recv, cnt, t, ncclSum, ncomm, ks), "ncclAllReduce");
+        break;
+      case Collective::AllGather:
+        nccl_check(api.AllGather(c.send, c.recv, cnt, t, ncomm, ks), "ncclAllGather");
+        break;
+      case Collective::ReduceScatter:
+        nccl_check(api.ReduceScatter(c.send, c.recv, cnt, t, ncclSum, ncomm, ks), "ncclReduceScatter");
+        break;
+      case Collective::AllToAll: {
+        const std::size_t bytes = cnt * elem_bytes(c.op.dtype);
+        nccl_check(api.GroupStart(), "group");
+        for (int p = 0; p < n; ++p) {
+          nccl_check(api.Send(static_cast<char*>(c.send) + p * bytes, cnt, t, p, ncomm, ks), "send");
+          nccl_check(api.Recv(static_cast<char*>(c.recv) + p * bytes, cnt, t, p, ncomm, ks), "recv");
+        }
+        nccl_check(api.GroupEnd(), "group");
+        break;
+      }
+    }
+  }
+
+  // One replay on this rank; returns [x_0..x_{N-1}, y_0..y_{M-1}, Z] in us.
+  std::vector<double> replay(Mode mode, const std::vector<CommConfig>* cfgs) {
+    const bool do_compute = mode != Mode::CommOnly;
+    const bool do_comm = mode != Mode::ComputeOnly;
+    const std::size_t M = dag.compute_ops.size(), N = comms.size();
+    coord.barrier();
+    const bool e2e = mode == Mode::LagomE2E;
+    cuda_check(cudaEventRecord(ev_start, cs), "record");
+    if (e2e && host_in)
+      cuda_check(cudaMemcpyAsync(gemms[0][0].A, host_in, opts.e2e_in_bytes, cudaMemcpyHostToDevice, cs), "h2d");
+    cuda_check(cudaStreamWaitEvent(ks, ev_start, 0), "wait");
+    if (do_compute) {
+      for (std::size_t i = 0; i < M; ++i) {
+        cuda_check(cudaEventRecord(ev_cb[i], cs), "record");
+        for (const Gemm& g : gemms[i]) launch_gemm(g);
+        cuda_check(cudaEventRecord(ev_ce[i], cs), "record");
+      }
+    }
+    if (do_comm) {
+      for (std::size_t j = 0; j < N; ++j) {
+        if (do_compute && comms[j].dep >= 0) cuda_check(cudaStreamWaitEvent(ks, ev_ce[comms[j].dep], 0), "wait");
+        cuda_check(cudaEventRecord(ev_kb[j], ks), "record");
+        if (mode == Mode::Nccl) launch_comm_nccl(comms[j]);
+        else launch_comm_lagom(comms[j], (*cfgs)[j]);
+        cuda_check(cudaEventRecord(ev_ke[j], ks), "record");
+      }
+    }
+    cuda_check(cudaEventRecord(ev_kend, ks), "record");
+    if (e2e && host_out) {
+      cuda_check(cudaStreamWaitEvent(cs, ev_kend, 0), "wait");
+      cuda_check(cudaMemcpyAsync(host_out, comms.back().recv, opts.e2e_out_bytes, cudaMemcpyDeviceToHost, cs), "d2h");
+    }
+    cuda_check(cudaEventRecord(ev_cend, cs), "record");
+    cuda_check(cudaEventSynchronize(ev_cend), "sync");
+    cuda_check(cudaEventSynchronize(ev_kend), "sync");
+    coll_check(lagom_comm_check(lcomm), "collective watchdog");
+
+    std::vector<double> out(N + M + 1, 0.0);
+    auto us = [](cudaEvent_t a, cudaEvent_t b) {
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+      return static_cast<double>(ms) * 1e3;
+    };
+    double z = 0.0;
+    if (do_comm)
+      for (std::size_t j = 0; j < N; ++j) out[j] = us(ev_kb[j], ev_ke[j]);
+    if (do_compute)
+      for (std::size_t i = 0; i < M; ++i) out[N + i] = us(ev_cb[i], ev_ce[i]);
+    z = std::max(us(ev_start, ev_cend), us(ev_start, ev_kend));
+    out[N + M] = z;
+    return out;
+  }
+
+  ReplayMeasurement measure(Mode mode, const std::vector<CommConfig>* cfgs) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (cfgs && cfgs->size() != comms.size())
+      throw Error(ErrorCode::InvalidWorkload, "configs",
+                  "expected " + std::to_string(comms.size()) + " configs, got " + std::to_string(cfgs->size()));
+    for (int w = 0; w < opts.warmup; ++w) replay(mode, cfgs);
+    const std::size_t N = comms.size(), M = dag.compute_ops.size();
+    std::vector<std::vector<double>> reps;
+    for (int r = 0; r < std::max(1, opts.repeats); ++r) {
+      std::vector<double> v = replay(mode, cfgs);
+      coord.allreduce_max(v.data(), v.size());
+      reps.push_back(std::move(v));
+    }
+    ReplayMeasurement m;
+    m.profile.comm_times.resize(N);
+    m.comp_times.resize(M);
+    std::vector<double> col(reps.size());
+    auto med = [&](std::size_t k) {
+      for (std::size_t r = 0; r < reps.size(); ++r) col[r] = reps[r][k];
+      return median_of(col);
+    };
+    for (std::size_t j = 0; j < N; ++j) m.profile.comm_times[j] = med(j);
+    for (std::size_t i = 0; i < M; ++i) m.comp_times[i] = med(N + i);
+    m.profile.total_comm = 0.0;
+    for (double x : m.profile.comm_times) m.profile.total_comm += x;
+    m.profile.total_compute = 0.0;
+    for (double y : m.comp_times) m.profile.total_compute += y;
+    m.profile.makespan = med(N + M);
+    ++calls;
+    m.wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    return m;
+  }
+
+  // rank-0 side of the command protocol
+  ReplayMeasurement remote(Mode mode, const std::vector<CommConfig>* cfgs) {
+    if (rank != 0) throw Error(ErrorCode::InvalidInput, "engine", "remote_* is rank 0 only");
+    std::vector<WireConfig> wire(comms.size() + 1);
+    wire[0].algorithm = static_cast<std::int32_t>(mode);
+    if (cfgs) {
+      if (cfgs->size() != comms.size())
+        throw Error(ErrorCode::InvalidWorkload, "configs", "one config per comm op expected");
+      for (std::size_t j = 0; j < cfgs->size(); ++j) {
+        const CommConfig& c = (*cfgs)[j];
+        wire[j + 1] = WireConfig{static_cast<std::int32_t>(c.algorithm), static_cast<std::int32_t>(c.protocol),
+                                 static_cast<std::int32_t>(c.transport), c.num_channels, c.num_threads, 0,
+                                 c.chunk_size};
+      }
+    }
+    coord.broadcast(wire.data(), wire.size() * sizeof(WireConfig), 0);
+    if (mode == Mode::Stop) return {};
+    return measure(mode, cfgs);
+  }
+};
+
+ReplayEngine::ReplayEngine(const ReplayDag& dag, Coordinator& coord, const ReplayOptions& opts)
+    : impl_(std::make_unique<Impl>(dag, coord, opts)) {}
+ReplayEngine::~ReplayEngine() = default;
+
+const ReplayDag& ReplayEngine::dag() const { return impl_->dag; }
+int ReplayEngine::rank() const { return impl_->rank; }
+int ReplayEngine::nranks() const { return impl_->n; }
+int ReplayEngine::calls() const { return impl_->calls; }
+
+ReplayMeasurement ReplayEngine::run(const std::vector<CommConfig>& configs) {
+  return impl_->measure(Mode::Lagom, &configs);
+}
+ReplayMeasurement ReplayEngine::run_e2e(const std::vector<CommConfig>& configs) {
+  return impl_->measure(Mode::LagomE2E, &configs);
+}
+ReplayMeasurement ReplayEngine::run_nccl() {
+  if (!impl_->ncomm) throw Error(ErrorCode::InvalidInput, "engine", "NCCL baseline disabled");
+  return impl_->measure(Mode::Nccl, nullptr);
+}
+ReplayMeasurement ReplayEngine::run_compute_only() { return impl_->measure(Mode::ComputeOnly, nullptr); }
+ReplayMeasurement ReplayEngine::run_comm_only(const std::vector<CommConfig>& configs) {
+  return impl_->measure(Mode::CommOnly, &configs);
+}
+
+void ReplayEngine::serve() {
+  Impl& I = *impl_;
+  if (I.rank == 0) return;
+  for (;;) {
+    std::vector<WireConfig> wire(I.comms.size() + 1);
+    I.coord.broadcast(wire.data(), wire.size() * sizeof(WireConfig), 0);
+    const Mode mode = static_cast<Mode>(wire[0].algorithm);
+    if (mode == Mode::Stop) return;
+    std::vector<CommConfig> cfgs(I.comms.size());
+    for (std::size_t j = 0; j < cfgs.size(); ++j) {
+      const WireConfig& w = wire[j + 1];
+      cfgs[j] = CommConfig{static_cast<Algorithm>(w.algorithm), static_cast<Protocol>(w.protocol),
+                           static_cast<Transport>(w.transport), w.num_channels, w.num_threads, w.chunk_size};
+    }
+    const bool with_cfg = mode == Mode::Lagom || mode == Mode::CommOnly || mode == Mode::LagomE2E;
+    I.measure(mode, with_cfg ? &cfgs : nullptr);
+  }
+}
+
+void ReplayEngine::stop() {
+  if (impl_->rank == 0 && impl_->n > 1) impl_->remote(Mode::Stop, nullptr);
+}
+ReplayMeasurement ReplayEngine::remote_run(const std::vector<CommConfig>& c) { return impl_->remote(Mode::Lagom, &c); }
+ReplayMeasurement ReplayEngine::remote_run_e2e(const std::vector<CommConfig>& c) {
+  return impl_->remote(Mode::LagomE2E, &c);
+}
+ReplayMeasurement ReplayEngine::remote_run_nccl() {
+  if (!impl_->ncomm) throw Error(ErrorCode::InvalidInput, "engine", "NCCL baseline disabled");
+  return impl_->remote(Mode::Nccl, nullptr);
+}
+ReplayMeasurement ReplayEngine::remote_run_compute_only() { return impl_->remote(Mode::ComputeOnly, nullptr); }
+ReplayMeasurement ReplayEngine::remote_run_comm_only(const std::vector<CommConfig>& c) {
+  return impl_->remote(Mode::CommOnly, &c);
+}
+
+// --------------------------------------------------------------- profilers --
+
+ProfileFn make_gpu_profiler(ReplayEngine& engine,
+                            std::vector<std::pair<std::vector<CommConfig>, ProfileResult>>* record) {
+  return [&engine, record](const std::vector<CommConfig>& configs) {
+    ReplayMeasurement m = engine.remote_run(configs);
+    if (record) record->emplace_back(configs, m.profile);
+    return m.profile;
+  };
+}
+
+ProfileFn make_table_profiler(std::vector<std::pair<std::vector<CommConfig>, ProfileResult>> table) {
+  auto shared = std::make_shared<decltype(table)>(std::move(table));
+  return [shared](const std::vector<CommConfig>& configs) -> ProfileResult {
+    for (const auto& [cfg, res] : *shared)
+      if (cfg == configs) return res;
+    throw Error(ErrorCode::InvalidInput, "profile_table", "no recorded entry for this config vector");
+  };
+}
+
+}  // namespace lagom::b200

@@ -1,0 +1,307 @@
+// Python bindings (pybind11) of the C++ API — used by tests/ and bench.py.
+// JSON in, JSON out, in the reference's own file formats (reference
+// docs/formats.md: workload / configs / params documents, tune-log records),
+// so everything Python sees is exactly what the reference CLI would emit.
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <chrono>
+#include <memory>
+
+#include "lagom/b200.hpp"
+#include "lagom/error.hpp"
+#include "lagom/json_io.hpp"
+#include "lagom/oracle.hpp"
+#include "lagom/simulator.hpp"
+#include "lagom/sweep.hpp"
+#include "lagom/tuner.hpp"
+#include "lagom/version.hpp"
+#include "lagom/workloads.hpp"
+
+namespace py = pybind11;
+using namespace lagom;
+using lagom::b200::ReplayDag;
+
+namespace {
+
+Json parse(const std::string& s) { return parse_json(s, "<python>"); }
+
+SubspaceParams params_or_default(const std::string& p) {
+  return p.empty() ? SubspaceParams::defaults() : params_from_json(parse(p));
+}
+
+Json profile_json(const ProfileResult& p) {
+  return Json{{"x", p.comm_times}, {"X", p.total_comm}, {"Y", p.total_compute}, {"Z", p.makespan}};
+}
+
+// Reference CLI seeds (lagom_main.cpp:181-198): min or nccl-default.
+std::vector<CommConfig> seed_configs(const Workload& w, const SubspaceParams& params,
+                                     const std::string& start) {
+  if (start != "min" && start != "nccl-default")
+    throw Error(ErrorCode::InvalidInput, "start", "expected min|nccl-default");
+  std::vector<CommConfig> out;
+  for (const CommOp& op : w.comm_ops) {
+    const StepBounds b = bounds_for(op, w.gpu);
+    CommConfig c = minimum_config(select_subspace(op, w.gpu, params), b);
+    if (start == "nccl-default") {
+      c.num_channels = std::min(8, b.nc_max);
+      c.num_threads = 512;
+      c.chunk_size = std::clamp<std::int64_t>(2048 * kKiB, b.c_min, b.c_max);
+    }
+    out.push_back(c);
+  }
+  return out;
+}
+
+// Tune log records in the reference CLI schema (lagom_main.cpp:204-236).
+Json tune_json(const Workload& w, const TuneResult& r, double wall_us) {
+  Json log = Json::array();
+  for (const TuneRecord& rec : r.log) {
+    Json j;
+    j["iter"] = rec.iteration;
+    j["comm_id"] = rec.comm_index ? Json(w.comm_ops[*rec.comm_index].id) : Json(nullptr);
+    j["config"] = rec.comm_index ? config_to_json(rec.config) : Json(nullptr);
+    j["x"] = rec.comm_index ? Json(rec.comm_time) : Json(nullptr);
+    j["X"] = rec.total_comm;
+    j["Y"] = rec.total_compute;
+    j["Z"] = rec.makespan;
+    Json h, done = Json::array();
+    for (std::size_t k = 0; k < rec.priorities.size(); ++k) {
+      h[w.comm_ops[k].id] = rec.priorities[k];
+      if (rec.done[k]) done.push_back(w.comm_ops[k].id);
+    }
+    j["H_table"] = h;
+    j["done"] = done;
+    if (rec.priority_after) j["H_after"] = *rec.priority_after;
+    else if (rec.comm_index) j["H_after"] = nullptr;
+    j["already_optimal"] = rec.already_optimal;
+    log.push_back(j);
+  }
+  Json states = Json::array();
+  for (const CommTuneState& s : r.states)
+    states.push_back({{"config", config_to_json(s.current)}, {"reason", to_string(s.reason)},
+                      {"done", s.done}, {"grown", s.grown}, {"priority", s.priority}});
+  return Json{{"configs", configs_to_json(r.configs)["configs"]},
+              {"final", profile_json(r.final_profile)},
+              {"initial_Z", r.initial_makespan},
+              {"profile_calls", r.profile_calls},
+              {"budget_exhausted", r.budget_exhausted},
+              {"boundary_condition", r.boundary_condition},
+              {"wall_us", wall_us},
+              {"log", log},
+              {"states", states}};
+}
+
+ReplayDag dag_from_json(const Json& d) {
+  ReplayDag dag;
+  dag.name = d.value("name", std::string("dag"));
+  for (const Json& c : d.at("compute_ops")) {
+    b200::ReplayComputeOp op;
+    op.id = c.at("id").get<std::string>();
+    for (const Json& g : c.at("gemms"))
+      op.gemms.push_back({g.at(0).get<std::int64_t>(), g.at(1).get<std::int64_t>(), g.at(2).get<std::int64_t>(),
+                          g.size() > 3 ? g.at(3).get<std::int64_t>() : 1});
+    dag.compute_ops.push_back(op);
+  }
+  for (const Json& c : d.at("comm_ops")) {
+    b200::ReplayCommOp op;
+    op.id = c.at("id").get<std::string>();
+    op.collective = collective_from_string(c.at("collective").get<std::string>());
+    op.dtype = c.value("dtype", 1);
+    op.count = c.at("count").get<std::int64_t>();
+    if (c.contains("ready_after") && !c["ready_after"].is_null())
+      op.ready_after = c["ready_after"].get<std::string>();
+    if (c.contains("bounds")) {
+      const Json& b = c["bounds"];
+      op.bounds.nc_max = b.value("nc_max", op.bounds.nc_max);
+      op.bounds.c_min = b.value("c_min", op.bounds.c_min);
+      op.bounds.c_max = b.value("c_max", op.bounds.c_max);
+    }
+    dag.comm_ops.push_back(op);
+  }
+  return dag;
+}
+
+GpuSpec gpu_from_json(const std::string& s) {
+  GpuSpec g;
+  if (s.empty()) return g;
+  const Json j = parse(s);
+  g.num_sms = j.value("num_sms", g.num_sms);
+  g.peak_mem_bw = j.value("peak_mem_bw", g.peak_mem_bw);
+  g.link_bw = j.value("link_bw", g.link_bw);
+  g.comm_bw_cap_fraction = j.value("comm_bw_cap_fraction", g.comm_bw_cap_fraction);
+  g.compute_on_comm_slowdown = j.value("compute_on_comm_slowdown", g.compute_on_comm_slowdown);
+  return g;
+}
+
+Json measurement_json(const b200::ReplayMeasurement& m) {
+  return Json{{"x", m.profile.comm_times}, {"y", m.comp_times}, {"X", m.profile.total_comm},
+              {"Y", m.profile.total_compute}, {"Z", m.profile.makespan}, {"wall_us", m.wall_us}};
+}
+
+std::vector<CommConfig> configs_arg(const std::string& s) { return configs_from_json(parse(s)); }
+
+class PyEngine {
+ public:
+  PyEngine(const std::string& dag_json, const std::string& coord_name, int rank, int size, int device,
+           int repeats, int warmup, bool nccl, std::int64_t max_chunk, int max_channels,
+           std::int64_t e2e_in, std::int64_t e2e_out)
+      : dag_(dag_from_json(parse(dag_json))) {
+    coord_ = b200::make_shm_coordinator(coord_name, rank, size);
+    b200::ReplayOptions o;
+    o.device = device;
+    o.repeats = repeats;
+    o.warmup = warmup;
+    o.enable_nccl = nccl;
+    o.max_chunk_bytes = max_chunk;
+    o.max_channels = max_channels;
+    o.e2e_in_bytes = e2e_in;
+    o.e2e_out_bytes = e2e_out;
+    engine_ = std::make_unique<b200::ReplayEngine>(dag_, *coord_, o);
+  }
+  std::string workload(const std::string& gpu_json) const {
+    return workload_to_json(b200::to_workload(dag_, gpu_from_json(gpu_json), coord_->size())).dump();
+  }
+  std::string run(const std::string& cfgs) {
+    py::gil_scoped_release nogil;
+    return measurement_json(engine_->remote_run(configs_arg(cfgs))).dump();
+  }
+  std::string run_e2e(const std::string& cfgs) {
+    py::gil_scoped_release nogil;
+    return measurement_json(engine_->remote_run_e2e(configs_arg(cfgs))).dump();
+  }
+  std::string run_nccl() {
+    py::gil_scoped_release nogil;
+    return measurement_json(engine_->remote_run_nccl()).dump();
+  }
+  std::string run_compute_only() {
+    py::gil_scoped_release nogil;
+    return measurement_json(engine_->remote_run_compute_only()).dump();
+  }
+  std::string run_comm_only(const std::string& cfgs) {
+    py::gil_scoped_release nogil;
+    return measurement_json(engine_->remote_run_comm_only(configs_arg(cfgs))).dump();
+  }
+  // Lagom search with the measured profiler (rank 0). Also returns the
+  // recorded profile table for bit-identical offline replays.
+  std::string tune(const std::string& gpu_json, const std::string& start, int budget,
+                   const std::string& params_json) {
+    py::gil_scoped_release nogil;
+    const Workload w = b200::to_workload(dag_, gpu_from_json(gpu_json), coord_->size());
+    const SubspaceParams params = params_or_default(params_json);
+    const std::vector<CommConfig> init = seed_configs(w, params, start);
+    std::vector<std::pair<std::vector<CommConfig>, ProfileResult>> table;
+    const auto t0 = std::chrono::steady_clock::now();
+    const TuneResult r = tune_impl(w, init, b200::make_gpu_profiler(*engine_, &table), budget);
+    const double wall = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    Json out = tune_json(w, r, wall);
+    out["initial"] = configs_to_json(init)["configs"];
+    Json tab = Json::array();
+    for (const auto& [cfg, res] : table)
+      tab.push_back({{"configs", configs_to_json(cfg)["configs"]}, {"result", profile_json(res)}});
+    out["profile_table"] = tab;
+    out["workload"] = workload_to_json(w);
+    return out.dump();
+  }
+  void serve() {
+    py::gil_scoped_release nogil;
+    engine_->serve();
+  }
+  void stop() { engine_->stop(); }
+  int rank() const { return engine_->rank(); }
+  int nranks() const { return engine_->nranks(); }
+  void barrier() {
+    py::gil_scoped_release nogil;
+    coord_->barrier();
+  }
+
+ private:
+  static TuneResult tune_impl(const Workload& w, const std::vector<CommConfig>& init, const ProfileFn& f,
+                              int budget) {
+    return lagom::tune(w, init, f, budget);
+  }
+  ReplayDag dag_;
+  std::unique_ptr<b200::Coordinator> coord_;
+  std::unique_ptr<b200::ReplayEngine> engine_;
+};
+
+}  // namespace
+
+PYBIND11_MODULE(_lagom_py, m) {
+  m.doc() = "lagom-b200 C++ API (JSON in/out in the reference formats)";
+  m.attr("version") = kVersion;
+  py::register_exception<Error>(m, "LagomError");
+
+  m.def("default_params", [] { return params_to_json(SubspaceParams::defaults()).dump(); });
+  m.def("gen", [](const std::string& pattern, int layers, std::uint64_t seed, int mcount, int ncount) {
+    Workload w;
+    if (pattern == "fsdp") w = gen_fsdp(layers, seed);
+    else if (pattern == "tp") w = gen_tp_domino(layers, seed);
+    else if (pattern == "ep") w = gen_ep_dualbatch(layers, seed);
+    else if (pattern == "allreduce-pair") w = gen_allreduce_pair();
+    else if (pattern == "random") w = gen_random(mcount, ncount, seed);
+    else throw Error(ErrorCode::InvalidInput, "pattern", "unknown pattern '" + pattern + "'");
+    return workload_to_json(w).dump();
+  }, py::arg("pattern"), py::arg("layers") = 4, py::arg("seed") = 1, py::arg("m") = 4, py::arg("n") = 2);
+  m.def("seed_configs", [](const std::string& w, const std::string& start, const std::string& p) {
+    return configs_to_json(seed_configs(workload_from_json(parse(w)), params_or_default(p), start)).dump();
+  }, py::arg("workload"), py::arg("start") = "min", py::arg("params") = "");
+  m.def("simulate", [](const std::string& w, const std::string& c, const std::string& p) {
+    const SimResult r = simulate(workload_from_json(parse(w)), configs_arg(c), params_or_default(p));
+    return Json{{"x", r.comm_times}, {"y", r.comp_times}, {"X", r.total_comm}, {"Y", r.total_compute},
+                {"Z", r.makespan}, {"trace", trace_to_json(r)}}.dump();
+  }, py::arg("workload"), py::arg("configs"), py::arg("params") = "");
+  m.def("tune_sim", [](const std::string& w, const std::string& start, int budget, const std::string& p) {
+    const Workload wl = workload_from_json(parse(w));
+    const SubspaceParams params = params_or_default(p);
+    const auto init = seed_configs(wl, params, start);
+    const auto t0 = std::chrono::steady_clock::now();
+    const TuneResult r = tune(wl, init, make_sim_profiler(wl, params), budget);
+    const double wall = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    Json out = tune_json(wl, r, wall);
+    out["initial"] = configs_to_json(init)["configs"];
+    return out.dump();
+  }, py::arg("workload"), py::arg("start") = "min", py::arg("budget") = 500, py::arg("params") = "");
+  m.def("tune_table", [](const std::string& w, const std::string& init, const std::string& table, int budget) {
+    const Workload wl = workload_from_json(parse(w));
+    std::vector<std::pair<std::vector<CommConfig>, ProfileResult>> t;
+    for (const Json& e : parse(table)) {
+      ProfileResult r;
+      r.comm_times = e["result"]["x"].get<std::vector<double>>();
+      r.total_comm = e["result"]["X"].get<double>();
+      r.total_compute = e["result"]["Y"].get<double>();
+      r.makespan = e["result"]["Z"].get<double>();
+      t.emplace_back(configs_from_json(e["configs"]), r);
+    }
+    const TuneResult r = tune(wl, configs_arg(init), b200::make_table_profiler(std::move(t)), budget);
+    return tune_json(wl, r, 0.0).dump();
+  }, py::arg("workload"), py::arg("initial"), py::arg("table"), py::arg("budget") = 500);
+  m.def("oracle", [](const std::string& w, const std::string& p, std::int64_t limit) {
+    const Workload wl = workload_from_json(parse(w));
+    const SubspaceParams params = params_or_default(p);
+    const OracleResult o = exhaustive(wl, default_grids(wl, params), params, limit);
+    return Json{{"Z", o.makespan}, {"evaluations", o.evaluations},
+                {"configs", configs_to_json(o.configs)["configs"]}}.dump();
+  }, py::arg("workload"), py::arg("params") = "", py::arg("limit") = 1000000);
+
+  py::class_<PyEngine>(m, "ReplayEngine")
+      .def(py::init<const std::string&, const std::string&, int, int, int, int, int, bool, std::int64_t, int,
+                    std::int64_t, std::int64_t>(),
+           py::arg("dag"), py::arg("coord_name"), py::arg("rank"), py::arg("size"), py::arg("device"),
+           py::arg("repeats") = 3, py::arg("warmup") = 1, py::arg("nccl") = true,
+           py::arg("max_chunk_bytes") = 4 << 20, py::arg("max_channels") = 32, py::arg("e2e_in_bytes") = 0,
+           py::arg("e2e_out_bytes") = 0)
+      .def("workload", &PyEngine::workload, py::arg("gpu") = "")
+      .def("run", &PyEngine::run)
+      .def("run_e2e", &PyEngine::run_e2e)
+      .def("run_nccl", &PyEngine::run_nccl)
+      .def("run_compute_only", &PyEngine::run_compute_only)
+      .def("run_comm_only", &PyEngine::run_comm_only)
+      .def("tune", &PyEngine::tune, py::arg("gpu") = "", py::arg("start") = "min", py::arg("budget") = 200,
+           py::arg("params") = "")
+      .def("serve", &PyEngine::serve)
+      .def("stop", &PyEngine::stop)
+      .def("barrier", &PyEngine::barrier)
+      .def_property_readonly("rank", &PyEngine::rank)
+      .def_property_readonly("nranks", &PyEngine::nranks);
+}

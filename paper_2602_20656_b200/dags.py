@@ -1,0 +1,174 @@
+"""Replay DAGs for BASELINE.json's configs 2-5.
+
+Each DAG is the reference Workload's overlap shape (ordered compute stream,
+serialized comm stream, ``ready_after`` gates — reference model.hpp:78-96 and
+the generator shapes of reference workloads.cpp:59-109) with real kernels
+attached: cuBLASLt bf16 GEMMs [m, n, k(, batch)] per compute op, and one
+collective per comm op (bf16, counts per include/lagom_coll.h). Shapes follow
+the public model cards; data is synthetic (random-init on device).
+
+``window`` builds the two-layer tuning window used to search configs: the
+layers of every config are identical, so a comm op's config found on the
+window is applied to the same comm role (bucket / position) in every layer of
+the full DAG, which the timed steps replay in full.
+"""
+from __future__ import annotations
+
+import json
+
+BF16 = 1
+MiB = 1 << 20
+
+
+def _attn_bwd(seq, d, heads_x_batch):
+    # dP = dO V^T (s,s,d); dV = P^T dO, dQ = dS K, dK = dS^T Q (s,d,s)
+    return [[seq, seq, d, heads_x_batch], [seq, d, seq, heads_x_batch],
+            [seq, d, seq, heads_x_batch], [seq, d, seq, heads_x_batch]]
+
+
+def _attn_fwd(seq, d, heads_x_batch):
+    return [[seq, seq, d, heads_x_batch], [seq, d, seq, heads_x_batch]]
+
+
+def gpt2_dp(nranks: int, layers: int = 24):
+    """Config 2 — GPT-2 1.3B, DP: layer backward + bucketed (25 MiB, DDP
+    default) gradient AllReduce gated on the layer's backward."""
+    h, T, s, d, heads, mb = 2048, 8192, 1024, 128, 16, 8
+    layer_params = 12 * h * h + 13 * h
+    layer_bytes = 2 * layer_params
+    bucket = 25 * MiB
+    gemms = [[T, 4 * h, h], [h, 4 * h, T],       # fc2 dgrad / wgrad
+             [T, h, 4 * h], [4 * h, h, T],       # fc1
+             [T, h, h], [h, h, T]]               # attention out-proj
+    gemms += _attn_bwd(s, d, heads * mb)          # attention core backward
+    gemms += [[T, h, 3 * h], [3 * h, h, T]]      # qkv
+    compute, comm = [], []
+    for l in range(layers):
+        compute.append({"id": f"bwd{l}", "gemms": gemms})
+        left, b = layer_bytes, 0
+        while left > 0:
+            nbytes = min(bucket, left)
+            comm.append({"id": f"ar{l}_{b}", "collective": "ALL_REDUCE", "dtype": BF16,
+                         "count": nbytes // 2, "ready_after": f"bwd{l}", "role": b})
+            left -= nbytes
+            b += 1
+    return {"name": f"gpt2-1.3b-dp{nranks}", "compute_ops": compute, "comm_ops": comm,
+            "flops_per_step": 0.0}
+
+
+def llama8b_tp_sp(nranks: int, layers: int = 32):
+    """Config 3 — Llama-3 8B, TP=n with sequence parallelism (forward):
+    per layer AG(seq-sharded activations) -> attention block -> RS, then
+    AG -> MLP -> RS, overlapped Domino-style (comms gated on the producing
+    compute, overlapping the next compute)."""
+    n = nranks
+    h, T, ffn, hd = 4096, 8192, 14336, 128
+    q_heads, kv_heads = 32, 8
+    shard = T // n
+    compute, comm = [], []
+    for l in range(layers):
+        qkv = (q_heads + 2 * kv_heads) * hd // n
+        attn = [[T, qkv, h]] + _attn_fwd(T, hd, max(1, q_heads // n)) + [[T, h, q_heads * hd // n]]
+        mlp = [[T, 2 * ffn // n, h], [T, h, ffn // n]]
+        compute.append({"id": f"attn{l}", "gemms": attn})
+        compute.append({"id": f"mlp{l}", "gemms": mlp})
+        comm.append({"id": f"rs_attn{l}", "collective": "REDUCE_SCATTER", "dtype": BF16,
+                     "count": shard * h, "ready_after": f"attn{l}", "role": 0})
+        comm.append({"id": f"ag_mlp{l}", "collective": "ALL_GATHER", "dtype": BF16,
+                     "count": shard * h, "ready_after": f"attn{l}", "role": 1})
+        comm.append({"id": f"rs_mlp{l}", "collective": "REDUCE_SCATTER", "dtype": BF16,
+                     "count": shard * h, "ready_after": f"mlp{l}", "role": 2})
+        comm.append({"id": f"ag_attn{l + 1}", "collective": "ALL_GATHER", "dtype": BF16,
+                     "count": shard * h, "ready_after": f"mlp{l}", "role": 3})
+    return {"name": f"llama3-8b-tp{n}-sp", "compute_ops": compute, "comm_ops": comm}
+
+
+def llama70b_fsdp(nranks: int, layers: int = 4):
+    """Config 4 — Llama-3 70B-shaped layers, FSDP/ZeRO-3 (fwd): per layer a
+    parameter AllGather (prefetched after the previous layer), the layer's
+    GEMMs, and the gradient ReduceScatter gated on it (reference gen_fsdp
+    shape, workloads.cpp:59-76)."""
+    n = nranks
+    h, T, ffn, hd = 8192, 4096, 28672, 128
+    q_heads, kv_heads = 64, 8
+    layer_params = h * (q_heads + 2 * kv_heads) * hd + q_heads * hd * h + 3 * h * ffn
+    shard = layer_params // n
+    compute, comm = [], []
+    for l in range(layers):
+        g = [[T, (q_heads + 2 * kv_heads) * hd, h]] + _attn_fwd(T, hd, q_heads) + \
+            [[T, h, q_heads * hd], [T, 2 * ffn, h], [T, h, ffn]]
+        ag = {"id": f"ag{l}", "collective": "ALL_GATHER", "dtype": BF16, "count": shard, "role": 0}
+        if l > 0:
+            ag["ready_after"] = f"layer{l - 1}"
+        comm.append(ag)
+        compute.append({"id": f"layer{l}", "gemms": g})
+        comm.append({"id": f"rs{l}", "collective": "REDUCE_SCATTER", "dtype": BF16, "count": shard,
+                     "ready_after": f"layer{l}", "role": 1})
+    return {"name": f"llama3-70b-layers-fsdp{n}", "compute_ops": compute, "comm_ops": comm}
+
+
+def mixtral_ep(nranks: int, layers: int = 32):
+    """Config 5 — Mixtral 8x7B, EP=n (dual micro-batch): per layer dispatch
+    AllToAll, expert GEMMs, combine AllToAll (reference gen_ep_dualbatch
+    shape, workloads.cpp:92-109). 4096 tokens x top-2 = 8192 slots/rank."""
+    n = nranks
+    h, ffn, slots = 4096, 14336, 8192
+    experts_per_rank = max(1, 8 // n)
+    compute, comm = [], []
+    per_peer = slots * h // n
+    for l in range(layers):
+        g = [[slots // experts_per_rank, 2 * ffn, h], [slots // experts_per_rank, h, ffn]] * experts_per_rank
+        disp = {"id": f"a2a_in{l}", "collective": "ALL_TO_ALL", "dtype": BF16, "count": per_peer, "role": 0}
+        if l > 0:
+            disp["ready_after"] = f"ex{l - 1}"
+        comm.append(disp)
+        compute.append({"id": f"ex{l}", "gemms": g})
+        comm.append({"id": f"a2a_out{l}", "collective": "ALL_TO_ALL", "dtype": BF16, "count": per_peer,
+                     "ready_after": f"ex{l}", "role": 1})
+    return {"name": f"mixtral-8x7b-ep{n}", "compute_ops": compute, "comm_ops": comm}
+
+
+BUILDERS = {"gpt2-1.3b-dp": gpt2_dp, "llama3-8b-tp-sp": llama8b_tp_sp,
+            "llama3-70b-fsdp": llama70b_fsdp, "mixtral-8x7b-ep": mixtral_ep}
+
+
+def window(dag: dict, layers: int = 2) -> dict:
+    """The tuning window: the first `layers` compute ops' layers and the comm
+    ops gated on them (plus ungated leading comms)."""
+    keep_compute = dag["compute_ops"][: layers * _compute_per_layer(dag)]
+    ids = {c["id"] for c in keep_compute}
+    last = keep_compute[-1]["id"]
+    comm = []
+    for c in dag["comm_ops"]:
+        if c.get("ready_after") is None or c["ready_after"] in ids:
+            if c.get("ready_after") == last:
+                continue  # would not overlap anything inside the window
+            comm.append(c)
+    return {"name": dag["name"] + "-window", "compute_ops": keep_compute, "comm_ops": comm}
+
+
+def _compute_per_layer(dag):
+    return 2 if dag["name"].startswith("llama3-8b") else 1
+
+
+def expand_configs(dag: dict, win: dict, win_configs: list) -> list:
+    """Map configs tuned on the window to every comm op of the full DAG by
+    comm role (bucket index / position in the layer)."""
+    by_role = {}
+    for c, cfg in zip(win["comm_ops"], win_configs):
+        by_role.setdefault(c.get("role", 0), cfg)
+    fallback = win_configs[0]
+    return [by_role.get(c.get("role", 0), fallback) for c in dag["comm_ops"]]
+
+
+def flops(dag: dict) -> float:
+    tot = 0.0
+    for c in dag["compute_ops"]:
+        for g in c["gemms"]:
+            b = g[3] if len(g) > 3 else 1
+            tot += 2.0 * g[0] * g[1] * g[2] * b
+    return tot
+
+
+def to_json(dag: dict) -> str:
+    return json.dumps(dag)
