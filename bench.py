@@ -14,7 +14,8 @@ stream, gated on its layer) through the native C++ replay engine. Timing is
 device-side (CUDA events on the engine's streams), max over ranks. The
 Lagom configs are searched first by the C++ tuner (tune(start=min), the
 reference's Alg. 1/2, bit-identical picks) with the GPU replay as its
-ProfileFn, on a two-layer window whose comm roles recur in every layer.
+ProfileFn replaying the full iteration; comm ops of one role (the k-th
+bucket of every layer) share a config.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -175,7 +176,8 @@ def main():
     ap.add_argument("--impl", default="lagom", choices=["lagom", "reference"])
     ap.add_argument("--workload", default="gpt2-1.3b-dp")
     ap.add_argument("--budget", type=int, default=120)
-    ap.add_argument("--start", default="min", choices=["min", "nccl-default"])
+    ap.add_argument("--start", default="best", choices=["min", "nccl-default", "best"],
+                    help="tune() seed (reference CLI --start); best = run both, keep the lower final Z")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default="")
@@ -208,55 +210,66 @@ def main():
                            "link_bw": NVLINK_PEER_GBS * 1e3, "comm_bw_cap_fraction": 0.6})
 
     dag = dags.BUILDERS[args.workload](world)
-    win = dags.window(dag)
+    # Comm roles recur in every layer; the last layer's comms are exposed (no
+    # compute left to hide them), so they get groups of their own.
+    last_compute = dag["compute_ops"][-1]["id"]
+    nroles = 1 + max(int(c.get("role", 0)) for c in dag["comm_ops"])
+    groups = [int(c.get("role", 0)) + (nroles if c.get("ready_after") == last_compute else 0)
+              for c in dag["comm_ops"]]
+    present = sorted(set(groups))
+    groups = [present.index(g) for g in groups]
 
-    # ---- 1. Lagom search on the tuning window (rank 0 drives, others serve)
-    t_tune = time.perf_counter()
-    eng = L.ReplayEngine(json.dumps(win), f"lagom_{token}_w", rank, world, local, repeats=3, warmup=1,
-                         nccl=False)
-    tuned = None
-    if rank == 0:
-        tuned = json.loads(eng.tune(gpu_json, args.start, args.budget, ""))
-        eng.stop()
-    else:
-        eng.serve()
-    del eng
-    tune_wall_s = time.perf_counter() - t_tune
-    if world > 1:
-        box = [tuned]
-        dist.broadcast_object_list(box, src=0)
-        tuned = box[0]
-    win_cfgs = tuned["configs"]
-    full_cfgs = dags.expand_configs(dag, win, win_cfgs)
-    seed_win = tuned["initial"]
-
-    # ---- 2. full-iteration replays
+    # One engine for the whole run: rank 0 drives (search + measured replays),
+    # the other ranks serve replay commands until rank 0 stops them.
     T_in_bytes = 8192 * 2048 * 2
-    eng = L.ReplayEngine(json.dumps(dag), f"lagom_{token}_f", rank, world, local, repeats=1, warmup=0,
+    eng = L.ReplayEngine(json.dumps(dag), f"lagom_{token}", rank, world, local, repeats=1, warmup=0,
                          nccl=not args.no_nccl, e2e_in_bytes=T_in_bytes, e2e_out_bytes=4096)
-    result = None
+    result, tuned, tune_wall_s = None, None, 0.0
     if rank != 0:
         eng.serve()
     else:
+        # ---- 1. Lagom search (C++ tune(), reference Alg. 1/2) with the GPU
+        # replay of the FULL iteration as ProfileFn; comm ops of the same role
+        # (k-th bucket of every layer) share one config.
+        t_tune = time.perf_counter()
+        eng.run_compute_only()  # first-touch / clocks settle before the search
+        starts = ["min", "nccl-default"] if args.start == "best" else [args.start]
+        runs = {st: json.loads(eng.tune(gpu_json, st, args.budget, "", groups)) for st in starts}
+        best_start = min(runs, key=lambda st: runs[st]["final"]["Z"])
+        tuned = runs[best_start]
+        tuned["start"] = best_start
+        tuned["other_starts"] = {st: {"Z": r["final"]["Z"], "calls": r["profile_calls"],
+                                      "boundary": r["boundary_condition"]}
+                                 for st, r in runs.items() if st != best_start}
+        tune_wall_s = time.perf_counter() - t_tune
+        full_cfgs = [tuned["configs"][g] for g in groups]
+        seed_full = [dict(tuned["initial"][g], num_channels=8, num_threads=512, chunk_size=2 << 20)
+                     for g in groups]
         cfg_doc = json.dumps({"configs": full_cfgs})
-        ncc = dags.expand_configs(dag, win, [dict(c, num_channels=min(8, 32), num_threads=512,
-                                                  chunk_size=2 << 20) for c in seed_win])
-        ncc_doc = json.dumps({"configs": ncc})
+        ncc_doc = json.dumps({"configs": seed_full})
 
         def series(fn, k):
             return [json.loads(fn()) for _ in range(k)]
 
-        series(lambda: eng.run(cfg_doc), args.warmup)
+        # ---- 2. measured full-iteration replays. The arms are interleaved
+        # step by step (lagom, nccl, seed, e2e, ...) so that clock/power drift
+        # of the power-capped part affects every arm alike.
+        arms = {"lagom": lambda: eng.run(cfg_doc), "e2e": lambda: eng.run_e2e(cfg_doc),
+                "seed": lambda: eng.run(ncc_doc)}
+        if not args.no_nccl:
+            arms["nccl"] = eng.run_nccl
+        for _ in range(args.warmup):
+            for fn in arms.values():
+                fn()
+        runs = {k: [] for k in arms}
         with ClockSampler(local) as clk:
-            lagom_runs = series(lambda: eng.run(cfg_doc), args.steps)
-        e2e_runs = series(lambda: eng.run_e2e(cfg_doc), args.steps)
+            for _ in range(args.steps):
+                for k, fn in arms.items():
+                    runs[k].append(json.loads(fn()))
+        lagom_runs, e2e_runs, seed_runs = runs["lagom"], runs["e2e"], runs["seed"]
+        nccl_runs = runs.get("nccl", [])
         compute_only = series(eng.run_compute_only, max(3, args.steps // 3))
         comm_only = series(lambda: eng.run_comm_only(cfg_doc), max(3, args.steps // 3))
-        seed_runs = series(lambda: eng.run(ncc_doc), max(3, args.steps // 2))
-        nccl_runs = []
-        if not args.no_nccl:
-            series(eng.run_nccl, 2)
-            nccl_runs = series(eng.run_nccl, args.steps)
         eng.stop()
         result = dict(lagom=lagom_runs, e2e=e2e_runs, compute=compute_only, comm=comm_only,
                       seed=seed_runs, nccl=nccl_runs, clocks=clk.summary())
@@ -324,11 +337,12 @@ def main():
         "config": {"workload": dag["name"], "compute_ops": len(dag["compute_ops"]),
                    "comm_ops": len(dag["comm_ops"]), "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
-                   "tune": {"start": args.start, "window_comm_ops": len(win["comm_ops"]),
+                   "tune": {"start": tuned["start"], "others": tuned["other_starts"],
+                            "groups": len(tuned["configs"]),
                             "profile_calls": tuned["profile_calls"], "boundary": tuned["boundary_condition"],
                             "search_wall_s": round(tune_wall_s, 3),
                             "picks": [f"{c['algorithm']}/{c['protocol']}/NC{c['num_channels']}/NT"
-                                      f"{c['num_threads']}/C{c['chunk_size'] // 1024}K" for c in win_cfgs]}},
+                                      f"{c['num_threads']}/C{c['chunk_size'] // 1024}K" for c in tuned["configs"]]}},
         "nccl_default_ms": ms_nccl,
         "speedup_vs_nccl_default": (ms_nccl / ms) if ms_nccl else None,
         "lagom_kernels_nccl_seed_ms": ms_seed,

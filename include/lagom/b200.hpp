@@ -157,6 +157,16 @@ class ReplayEngine {
 ProfileFn make_gpu_profiler(ReplayEngine& engine,
                             std::vector<std::pair<std::vector<CommConfig>, ProfileResult>>* record = nullptr);
 
+// Role-tied search: comm ops with the same group id share one config (e.g.
+// the k-th gradient bucket of every layer). The tuner sees one comm op per
+// group (grouped_workload); the profiler replays the FULL DAG with the group
+// configs expanded to every op and reports x_g = sum of its ops' x_j, so X,
+// Y and Z are those of the real iteration.
+Workload grouped_workload(const ReplayDag& dag, const std::vector<int>& group_of_op, const GpuSpec& gpu,
+                          int nranks);
+ProfileFn make_grouped_gpu_profiler(ReplayEngine& engine, std::vector<int> group_of_op,
+                                    std::vector<std::pair<std::vector<CommConfig>, ProfileResult>>* record = nullptr);
+
 // A ProfileFn that answers from a recorded table (exact config-vector match;
 // throws Error(InvalidInput) on a miss). Used to prove that two tuners make
 // identical picks given the same profile table.

@@ -568,6 +568,43 @@ ProfileFn make_gpu_profiler(ReplayEngine& engine,
   };
 }
 
+Workload grouped_workload(const ReplayDag& dag, const std::vector<int>& group_of_op, const GpuSpec& gpu,
+                          int nranks) {
+  if (group_of_op.size() != dag.comm_ops.size())
+    throw Error(ErrorCode::InvalidInput, "groups", "one group id per comm op expected");
+  const Workload full = to_workload(dag, gpu, nranks);
+  Workload w;
+  w.gpu = full.gpu;
+  w.compute_ops = full.compute_ops;
+  const int groups = group_of_op.empty() ? 0 : *std::max_element(group_of_op.begin(), group_of_op.end()) + 1;
+  for (int g = 0; g < groups; ++g) {
+    const auto it = std::find(group_of_op.begin(), group_of_op.end(), g);
+    if (it == group_of_op.end()) throw Error(ErrorCode::InvalidInput, "groups", "group ids must be dense");
+    CommOp op = full.comm_ops[static_cast<std::size_t>(it - group_of_op.begin())];
+    op.id = "group" + std::to_string(g) + ":" + op.id;
+    w.comm_ops.push_back(op);
+  }
+  return w;
+}
+
+ProfileFn make_grouped_gpu_profiler(ReplayEngine& engine, std::vector<int> group_of_op,
+                                    std::vector<std::pair<std::vector<CommConfig>, ProfileResult>>* record) {
+  return [&engine, groups = std::move(group_of_op), record](const std::vector<CommConfig>& gcfg) {
+    std::vector<CommConfig> full(groups.size());
+    for (std::size_t j = 0; j < groups.size(); ++j) full[j] = gcfg.at(static_cast<std::size_t>(groups[j]));
+    const ReplayMeasurement m = engine.remote_run(full);
+    ProfileResult r;
+    r.comm_times.assign(gcfg.size(), 0.0);
+    for (std::size_t j = 0; j < groups.size(); ++j) r.comm_times[static_cast<std::size_t>(groups[j])] += m.profile.comm_times[j];
+    r.total_comm = 0.0;
+    for (double x : r.comm_times) r.total_comm += x;
+    r.total_compute = m.profile.total_compute;
+    r.makespan = m.profile.makespan;
+    if (record) record->emplace_back(gcfg, r);
+    return r;
+  };
+}
+
 ProfileFn make_table_profiler(std::vector<std::pair<std::vector<CommConfig>, ProfileResult>> table) {
   auto shared = std::make_shared<decltype(table)>(std::move(table));
   return [shared](const std::vector<CommConfig>& configs) -> ProfileResult {

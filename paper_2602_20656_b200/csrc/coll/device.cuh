@@ -472,11 +472,25 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
   return true;
 }
 
-// Plain local copy by a group (own block of AllToAll / single-rank cases).
+// Plain local copy by a group (own block of AllToAll / single-rank cases):
+// 8 x 16 B loads in flight per thread when both sides are 16 B aligned.
 __device__ __forceinline__ void group_copy(const Grp& g, const char* src, char* dst, int64_t nbytes) {
+  constexpr int U = 8;
   const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-  const int64_t units = (nbytes + 15) >> 4;
-  for (int64_t u = g.tid; u < units; u += g.n) {
+  const int64_t units = (nbytes + 15) >> 4, whole = nbytes >> 4;
+  int64_t u0 = g.tid;
+  if (al) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (; u0 + static_cast<int64_t>(U - 1) * g.n < whole; u0 += static_cast<int64_t>(g.n) * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) v[k] = s4[u0 + static_cast<int64_t>(k) * g.n];
+#pragma unroll
+      for (int k = 0; k < U; ++k) d4[u0 + static_cast<int64_t>(k) * g.n] = v[k];
+    }
+  }
+  for (int64_t u = u0; u < units; u += g.n) {
     const int nb = static_cast<int>(lmin(16, nbytes - u * 16));
     store_user(dst + u * 16, load_user(src + u * 16, nb, al), nb, al);
   }

@@ -185,14 +185,19 @@ class PyEngine {
   // Lagom search with the measured profiler (rank 0). Also returns the
   // recorded profile table for bit-identical offline replays.
   std::string tune(const std::string& gpu_json, const std::string& start, int budget,
-                   const std::string& params_json) {
+                   const std::string& params_json, const std::vector<int>& groups) {
     py::gil_scoped_release nogil;
-    const Workload w = b200::to_workload(dag_, gpu_from_json(gpu_json), coord_->size());
+    const GpuSpec gpu = gpu_from_json(gpu_json);
+    const bool grouped = !groups.empty();
+    const Workload w = grouped ? b200::grouped_workload(dag_, groups, gpu, coord_->size())
+                               : b200::to_workload(dag_, gpu, coord_->size());
     const SubspaceParams params = params_or_default(params_json);
     const std::vector<CommConfig> init = seed_configs(w, params, start);
     std::vector<std::pair<std::vector<CommConfig>, ProfileResult>> table;
+    const ProfileFn f = grouped ? b200::make_grouped_gpu_profiler(*engine_, groups, &table)
+                                : b200::make_gpu_profiler(*engine_, &table);
     const auto t0 = std::chrono::steady_clock::now();
-    const TuneResult r = tune_impl(w, init, b200::make_gpu_profiler(*engine_, &table), budget);
+    const TuneResult r = tune_impl(w, init, f, budget);
     const double wall = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     Json out = tune_json(w, r, wall);
     out["initial"] = configs_to_json(init)["configs"];
@@ -284,6 +289,28 @@ PYBIND11_MODULE(_lagom_py, m) {
                 {"configs", configs_to_json(o.configs)["configs"]}}.dump();
   }, py::arg("workload"), py::arg("params") = "", py::arg("limit") = 1000000);
 
+  // Exercises the native shm coordinator (CPU only): barrier, broadcast from
+  // rank 0, all-gather of rank ids, max-reduction. Used by the world_size-2
+  // CPU tests of the multi-rank host path.
+  m.def("coord_selftest", [](const std::string& name, int rank, int size, int rounds) {
+    py::gil_scoped_release nogil;
+    auto c = b200::make_shm_coordinator(name, rank, size, 60.0);
+    Json out = Json::array();
+    for (int k = 0; k < rounds; ++k) {
+      c->barrier();
+      char msg[32] = {0};
+      if (rank == 0) std::snprintf(msg, sizeof msg, "round-%d-of-%d", k, size);
+      c->broadcast(msg, sizeof msg, 0);
+      std::int64_t mine = 100 * rank + k, all[8] = {0};
+      c->allgather(&mine, sizeof mine, all);
+      double v[3] = {static_cast<double>(rank), -static_cast<double>(rank), 1.5 * rank + k};
+      c->allreduce_max(v, 3);
+      out.push_back({{"msg", std::string(msg)}, {"gathered", std::vector<std::int64_t>(all, all + size)},
+                     {"max", std::vector<double>(v, v + 3)}});
+    }
+    return out.dump();
+  }, py::arg("name"), py::arg("rank"), py::arg("size"), py::arg("rounds") = 3);
+
   py::class_<PyEngine>(m, "ReplayEngine")
       .def(py::init<const std::string&, const std::string&, int, int, int, int, int, bool, std::int64_t, int,
                     std::int64_t, std::int64_t>(),
@@ -298,7 +325,7 @@ PYBIND11_MODULE(_lagom_py, m) {
       .def("run_compute_only", &PyEngine::run_compute_only)
       .def("run_comm_only", &PyEngine::run_comm_only)
       .def("tune", &PyEngine::tune, py::arg("gpu") = "", py::arg("start") = "min", py::arg("budget") = 200,
-           py::arg("params") = "")
+           py::arg("params") = "", py::arg("groups") = std::vector<int>{})
       .def("serve", &PyEngine::serve)
       .def("stop", &PyEngine::stop)
       .def("barrier", &PyEngine::barrier)
