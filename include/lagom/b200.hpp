@@ -142,8 +142,11 @@ class ReplayEngine {
   ReplayMeasurement remote_run_compute_only();                               // rank 0 only
   ReplayMeasurement remote_run_comm_only(const std::vector<CommConfig>& c);  // rank 0 only
 
-  // Number of profile calls served and the accumulated GPU time of replays.
+  // Number of replay measurements performed.
   int calls() const;
+  // Rank 0: replays per measurement and unrecorded warmups for the following
+  // remote_* calls (sent along with each command to the serving ranks).
+  void set_measurement(int repeats, int warmup);
 
  private:
   struct Impl;

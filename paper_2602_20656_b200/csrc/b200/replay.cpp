@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -65,6 +67,19 @@ ncclDataType_t nccl_type(int dtype) {
     case LAGOM_F16: return ncclFloat16;
     default: return ncclInt32;
   }
+}
+
+// LAGOM_TRACE=1: one stderr line per measurement / command, per rank.
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LAGOM_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
 }
 
 enum class Mode : int { Lagom = 1, Nccl = 2, ComputeOnly = 3, CommOnly = 4, Stop = 5, LagomE2E = 6 };
@@ -445,14 +460,21 @@ struct ReplayEngine::Impl {
   }
 
   ReplayMeasurement measure(Mode mode, const std::vector<CommConfig>* cfgs) {
+    return measure(mode, cfgs, opts.repeats, opts.warmup);
+  }
+
+  ReplayMeasurement measure(Mode mode, const std::vector<CommConfig>* cfgs, int repeats, int warmup) {
     const auto t0 = std::chrono::steady_clock::now();
+    if (trace_on())
+      std::fprintf(stderr, "[lagom rank %d %.3f] measure mode=%d repeats=%d warmup=%d\n", rank, now_s(),
+                   static_cast<int>(mode), repeats, warmup);
     if (cfgs && cfgs->size() != comms.size())
       throw Error(ErrorCode::InvalidWorkload, "configs",
                   "expected " + std::to_string(comms.size()) + " configs, got " + std::to_string(cfgs->size()));
-    for (int w = 0; w < opts.warmup; ++w) replay(mode, cfgs);
+    for (int w = 0; w < warmup; ++w) replay(mode, cfgs);
     const std::size_t N = comms.size(), M = dag.compute_ops.size();
     std::vector<std::vector<double>> reps;
-    for (int r = 0; r < std::max(1, opts.repeats); ++r) {
+    for (int r = 0; r < std::max(1, repeats); ++r) {
       std::vector<double> v = replay(mode, cfgs);
       coord.allreduce_max(v.data(), v.size());
       reps.push_back(std::move(v));
@@ -474,6 +496,9 @@ struct ReplayEngine::Impl {
     m.profile.makespan = med(N + M);
     ++calls;
     m.wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    if (trace_on())
+      std::fprintf(stderr, "[lagom rank %d %.3f] done mode=%d Z=%.1fus wall=%.1fms\n", rank, now_s(),
+                   static_cast<int>(mode), m.profile.makespan, m.wall_us / 1e3);
     return m;
   }
 
@@ -482,6 +507,8 @@ struct ReplayEngine::Impl {
     if (rank != 0) throw Error(ErrorCode::InvalidInput, "engine", "remote_* is rank 0 only");
     std::vector<WireConfig> wire(comms.size() + 1);
     wire[0].algorithm = static_cast<std::int32_t>(mode);
+    wire[0].protocol = opts.repeats;  // measurement settings travel with the command
+    wire[0].transport = opts.warmup;
     if (cfgs) {
       if (cfgs->size() != comms.size())
         throw Error(ErrorCode::InvalidWorkload, "configs", "one config per comm op expected");
@@ -494,7 +521,7 @@ struct ReplayEngine::Impl {
     }
     coord.broadcast(wire.data(), wire.size() * sizeof(WireConfig), 0);
     if (mode == Mode::Stop) return {};
-    return measure(mode, cfgs);
+    return measure(mode, cfgs, opts.repeats, opts.warmup);
   }
 };
 
@@ -506,6 +533,10 @@ const ReplayDag& ReplayEngine::dag() const { return impl_->dag; }
 int ReplayEngine::rank() const { return impl_->rank; }
 int ReplayEngine::nranks() const { return impl_->n; }
 int ReplayEngine::calls() const { return impl_->calls; }
+void ReplayEngine::set_measurement(int repeats, int warmup) {
+  impl_->opts.repeats = std::max(1, repeats);
+  impl_->opts.warmup = std::max(0, warmup);
+}
 
 ReplayMeasurement ReplayEngine::run(const std::vector<CommConfig>& configs) {
   return impl_->measure(Mode::Lagom, &configs);
@@ -537,7 +568,7 @@ void ReplayEngine::serve() {
                            static_cast<Transport>(w.transport), w.num_channels, w.num_threads, w.chunk_size};
     }
     const bool with_cfg = mode == Mode::Lagom || mode == Mode::CommOnly || mode == Mode::LagomE2E;
-    I.measure(mode, with_cfg ? &cfgs : nullptr);
+    I.measure(mode, with_cfg ? &cfgs : nullptr, wire[0].protocol, wire[0].transport);
   }
 }
 

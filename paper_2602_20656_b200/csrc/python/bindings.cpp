@@ -163,6 +163,7 @@ class PyEngine {
     return workload_to_json(b200::to_workload(dag_, gpu_from_json(gpu_json), coord_->size())).dump();
   }
   std::string run(const std::string& cfgs) {
+    alive();
     py::gil_scoped_release nogil;
     return measurement_json(engine_->remote_run(configs_arg(cfgs))).dump();
   }
@@ -213,6 +214,12 @@ class PyEngine {
     engine_->serve();
   }
   void stop() { engine_->stop(); }
+  // Collective: every rank must call it (NCCL communicator teardown).
+  void close() {
+    py::gil_scoped_release nogil;
+    engine_.reset();
+  }
+  void set_measurement(int repeats, int warmup) { engine_->set_measurement(repeats, warmup); }
   int rank() const { return engine_->rank(); }
   int nranks() const { return engine_->nranks(); }
   void barrier() {
@@ -221,6 +228,9 @@ class PyEngine {
   }
 
  private:
+  void alive() const {
+    if (!engine_) throw Error(ErrorCode::InvalidInput, "engine", "engine is closed");
+  }
   static TuneResult tune_impl(const Workload& w, const std::vector<CommConfig>& init, const ProfileFn& f,
                               int budget) {
     return lagom::tune(w, init, f, budget);
@@ -328,6 +338,8 @@ PYBIND11_MODULE(_lagom_py, m) {
            py::arg("params") = "", py::arg("groups") = std::vector<int>{})
       .def("serve", &PyEngine::serve)
       .def("stop", &PyEngine::stop)
+      .def("close", &PyEngine::close)
+      .def("set_measurement", &PyEngine::set_measurement, py::arg("repeats"), py::arg("warmup") = 0)
       .def("barrier", &PyEngine::barrier)
       .def_property_readonly("rank", &PyEngine::rank)
       .def_property_readonly("nranks", &PyEngine::nranks);
