@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--start", default="best", choices=["min", "nccl-default", "best"],
                     help="tune() seed (reference CLI --start); best = run both, keep the lower final Z")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--sm-reserve", type=int, default=1,
+                    help="Lagom replays run GEMMs on num_sms - max NC SMs (cuBLASLt SM count target)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -223,8 +225,9 @@ def main():
     # the other ranks serve replay commands until rank 0 stops them.
     T_in_bytes = 8192 * 2048 * 2
     eng = L.ReplayEngine(json.dumps(dag), f"lagom_{token}", rank, world, local, repeats=1, warmup=0,
-                         nccl=not args.no_nccl, e2e_in_bytes=T_in_bytes, e2e_out_bytes=4096)
-    result, tuned, tune_wall_s = None, None, 0.0
+                         nccl=not args.no_nccl, e2e_in_bytes=T_in_bytes, e2e_out_bytes=4096,
+                         reserve_comm_sms=bool(args.sm_reserve))
+    result, tuned, tune_wall_s, tune_runs = None, None, 0.0, {}
     if rank != 0:
         eng.serve()
     else:
@@ -245,6 +248,7 @@ def main():
             for st in runs:
                 zsel[st].append(json.loads(eng.run(docs[st]))["Z"])
         best_start = min(runs, key=lambda st: statistics.median(zsel[st]) if zsel[st] else 0.0)
+        tune_runs = runs
         tuned = runs[best_start]
         tuned["start"] = best_start
         tuned["other_starts"] = {st: {"Z_tune": r["final"]["Z"], "Z_select": zsel[st], "calls": r["profile_calls"],
@@ -345,6 +349,7 @@ def main():
         "config": {"workload": dag["name"], "compute_ops": len(dag["compute_ops"]),
                    "comm_ops": len(dag["comm_ops"]), "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
+                   "sm_partition": "GEMMs on num_sms - max NC" if args.sm_reserve else "none",
                    "tune": {"start": tuned["start"], "others": tuned["other_starts"],
                             "groups": len(tuned["configs"]),
                             "profile_calls": tuned["profile_calls"], "boundary": tuned["boundary_condition"],
@@ -367,7 +372,7 @@ def main():
     print(json.dumps(line), flush=True)
     if args.out:
         with open(args.out, "w") as f:
-            json.dump({"line": line, "tune": tuned, "raw": result}, f)
+            json.dump({"line": line, "tune": tuned, "tune_runs": tune_runs, "raw": result}, f)
 
 
 if __name__ == "__main__":

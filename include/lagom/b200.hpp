@@ -100,6 +100,11 @@ struct ReplayOptions {
   // result back to pinned host memory; both copies are inside Z.
   std::int64_t e2e_in_bytes = 0;
   std::int64_t e2e_out_bytes = 0;
+  // SM partition: in Lagom modes the GEMMs run with cuBLASLt's SM count
+  // target = num_sms - max NC of the configs, so collective CTAs never
+  // queue behind persistent GEMM CTAs (NCCL-baseline replays keep cuBLASLt's
+  // default). This is the contention model's lambda - NC made explicit.
+  bool reserve_comm_sms = false;
 };
 
 // One measured replay, max over ranks (median over repeats).

@@ -78,6 +78,11 @@ typedef struct {
    *   REDUCE_SCATTER send[nranks*count]   -> recv[count]
    *   ALL_TO_ALL     send[nranks*count]   -> recv[nranks*count]            */
   int64_t count;
+  /* Optional device pointer to two uint64 {first CTA start, last CTA end}
+   * (%globaltimer, ns), combined with atomicMin/atomicMax: initialise to
+   * {UINT64_MAX, 0}. The kernel's active span, excluding time the launch
+   * spent queued behind other kernels — what the cost model calls x. */
+  void* span_out;
 } lagom_coll_args_t;
 
 typedef struct lagom_comm* lagom_comm_t;

@@ -58,7 +58,8 @@ class _Args(ctypes.Structure):
     _fields_ = [("collective", ctypes.c_int), ("algorithm", ctypes.c_int),
                 ("protocol", ctypes.c_int), ("num_channels", ctypes.c_int),
                 ("num_threads", ctypes.c_int), ("chunk_bytes", ctypes.c_int64),
-                ("dtype", ctypes.c_int), ("redop", ctypes.c_int), ("count", ctypes.c_int64)]
+                ("dtype", ctypes.c_int), ("redop", ctypes.c_int), ("count", ctypes.c_int64),
+                ("span_out", ctypes.c_void_p)]
 
 
 EXPORTED_SYMBOLS = (
@@ -136,12 +137,12 @@ class CollConfig:
 
 def make_args(collective: int, cfg: CollConfig, dtype: int, count: int, redop: int = SUM) -> _Args:
     return _Args(collective, cfg.algorithm, cfg.protocol, cfg.num_channels, cfg.num_threads,
-                 cfg.chunk_size, dtype, redop, count)
+                 cfg.chunk_size, dtype, redop, count, None)
 
 
 def coll_bytes(collective: int, dtype: int, count: int, nranks: int) -> tuple[int, float]:
     """(algorithmic bytes S, busbw factor) per nccl-tests accounting."""
-    a = _Args(collective, 0, 0, 1, 64, 1024, dtype, 0, count)
+    a = _Args(collective, 0, 0, 1, 64, 1024, dtype, 0, count, None)
     s, f = ctypes.c_int64(), ctypes.c_double()
     _check(library().lagom_coll_bytes(ctypes.byref(a), nranks, ctypes.byref(s), ctypes.byref(f)))
     return s.value, f.value

@@ -84,12 +84,18 @@ double now_s() {
 
 enum class Mode : int { Lagom = 1, Nccl = 2, ComputeOnly = 3, CommOnly = 4, Stop = 5, LagomE2E = 6 };
 
+struct Plan {
+  cublasLtMatmulDesc_t desc = nullptr;
+  cublasLtMatmulAlgo_t algo{};
+};
+
 struct Gemm {
   GemmShape shape;
   cublasLtMatmulDesc_t desc = nullptr;
   cublasLtMatrixLayout_t a = nullptr, b = nullptr, d = nullptr;
   cublasLtMatmulAlgo_t algo{};
   void *A = nullptr, *B = nullptr, *D = nullptr;
+  std::map<int, Plan> by_sm_target;  // plans restricted to a number of SMs
 };
 
 struct Comm {
@@ -172,6 +178,7 @@ struct ReplayEngine::Impl {
   Coordinator& coord;
   ReplayOptions opts;
   int rank = 0, n = 1;
+  int num_sms = 148;
   cudaStream_t cs = nullptr, ks = nullptr;
   cublasLtHandle_t lt = nullptr;
   void* workspace = nullptr;
@@ -182,6 +189,8 @@ struct ReplayEngine::Impl {
   ncclComm_t ncomm = nullptr;
   cudaEvent_t ev_start = nullptr, ev_cend = nullptr, ev_kend = nullptr;
   std::vector<cudaEvent_t> ev_cb, ev_ce, ev_kb, ev_ke;
+  unsigned long long* spans = nullptr;  // device: [start_j...][end_j...]
+  std::vector<unsigned long long> spans_host;
   void* host_in = nullptr;   // pinned
   void* host_out = nullptr;  // pinned
   int calls = 0;
@@ -190,6 +199,7 @@ struct ReplayEngine::Impl {
     rank = coord.rank();
     n = coord.size();
     cuda_check(cudaSetDevice(opts.device), "cudaSetDevice");
+    cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, opts.device), "sm count");
     cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking), "stream");
     lt_check(cublasLtCreate(&lt), "cublasLtCreate");
@@ -223,6 +233,10 @@ struct ReplayEngine::Impl {
       opts.e2e_out_bytes = std::min<std::int64_t>(opts.e2e_out_bytes, last.out_elems * elem_bytes(last.op.dtype));
       cuda_check(cudaHostAlloc(&host_out, opts.e2e_out_bytes, cudaHostAllocDefault), "pinned out");
     }
+    if (!comms.empty()) {
+      cuda_check(cudaMalloc(&spans, 2 * comms.size() * sizeof(unsigned long long)), "spans");
+      spans_host.resize(2 * comms.size());
+    }
     cuda_check(cudaDeviceSynchronize(), "init sync");
     coord.barrier();
   }
@@ -232,6 +246,7 @@ struct ReplayEngine::Impl {
     cudaDeviceSynchronize();
     for (auto& ops : gemms)
       for (Gemm& g : ops) {
+        for (auto& [t, pl] : g.by_sm_target) cublasLtMatmulDescDestroy(pl.desc);
         if (g.desc) cublasLtMatmulDescDestroy(g.desc);
         if (g.a) cublasLtMatrixLayoutDestroy(g.a);
         if (g.b) cublasLtMatrixLayoutDestroy(g.b);
@@ -244,6 +259,7 @@ struct ReplayEngine::Impl {
       cudaFree(c.send);
       cudaFree(c.recv);
     }
+    if (spans) cudaFree(spans);
     if (host_in) cudaFreeHost(host_in);
     if (host_out) cudaFreeHost(host_out);
     if (ncomm) nccl().CommDestroy(ncomm);
@@ -358,14 +374,44 @@ struct ReplayEngine::Impl {
     }
   }
 
-  void launch_gemm(const Gemm& g) {
+  // A plan for `sm_target` SMs (0 = the whole GPU): the SM partition that
+  // leaves the collective's NC channels their own SMs (the contention
+  // model's lambda - NC). Cached per target.
+  const Plan& plan_for(Gemm& g, int sm_target) {
+    auto it = g.by_sm_target.find(sm_target);
+    if (it != g.by_sm_target.end()) return it->second;
+    Plan p;
+    lt_check(cublasLtMatmulDescCreate(&p.desc, CUBLAS_COMPUTE_32F, CUDA_R_32F), "desc");
+    const cublasOperation_t opA = CUBLAS_OP_T, opB = CUBLAS_OP_N;
+    lt_check(cublasLtMatmulDescSetAttribute(p.desc, CUBLASLT_MATMUL_DESC_TRANSA, &opA, sizeof opA), "transa");
+    lt_check(cublasLtMatmulDescSetAttribute(p.desc, CUBLASLT_MATMUL_DESC_TRANSB, &opB, sizeof opB), "transb");
+    const int32_t target = sm_target;
+    lt_check(cublasLtMatmulDescSetAttribute(p.desc, CUBLASLT_MATMUL_DESC_SM_COUNT_TARGET, &target, sizeof target),
+             "sm target");
+    cublasLtMatmulPreference_t pref;
+    lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
+    lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &workspace_bytes,
+                                                  sizeof workspace_bytes),
+             "pref ws");
+    cublasLtMatmulHeuristicResult_t res{};
+    int found = 0;
+    lt_check(cublasLtMatmulAlgoGetHeuristic(lt, p.desc, g.a, g.b, g.d, g.d, pref, 1, &res, &found), "heuristic");
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for the SM target");
+    p.algo = res.algo;
+    return g.by_sm_target.emplace(sm_target, p).first->second;
+  }
+
+  void launch_gemm(Gemm& g, int sm_target) {
     const float alpha = 1.0f, beta = 0.0f;
-    lt_check(cublasLtMatmul(lt, g.desc, &alpha, g.A, g.a, g.B, g.b, &beta, g.D, g.d, g.D, g.d, &g.algo,
-                            workspace, workspace_bytes, cs),
+    const cublasLtMatmulDesc_t desc = sm_target > 0 ? plan_for(g, sm_target).desc : g.desc;
+    const cublasLtMatmulAlgo_t* algo = sm_target > 0 ? &plan_for(g, sm_target).algo : &g.algo;
+    lt_check(cublasLtMatmul(lt, desc, &alpha, g.A, g.a, g.B, g.b, &beta, g.D, g.d, g.D, g.d, algo, workspace,
+                            workspace_bytes, cs),
              "cublasLtMatmul");
   }
 
-  void launch_comm_lagom(const Comm& c, const CommConfig& cfg) {
+  void launch_comm_lagom(const Comm& c, const CommConfig& cfg, unsigned long long* span) {
     lagom_coll_args_t a{};
     a.collective = coll_code(c.op.collective);
     a.algorithm = cfg.algorithm == Algorithm::Tree ? LAGOM_TREE : LAGOM_RING;
@@ -376,6 +422,7 @@ struct ReplayEngine::Impl {
     a.dtype = c.op.dtype;
     a.redop = LAGOM_SUM;
     a.count = c.op.count;
+    a.span_out = span;
     coll_check(lagom_coll_launch(lcomm, &a, c.send, c.recv, ks), c.op.id.c_str());
   }
 
@@ -409,6 +456,14 @@ struct ReplayEngine::Impl {
   // One replay on this rank; returns [x_0..x_{N-1}, y_0..y_{M-1}, Z] in us.
   std::vector<double> replay(Mode mode, const std::vector<CommConfig>* cfgs) {
     const bool do_compute = mode != Mode::CommOnly;
+    // SM partition (opts.reserve_comm_sms): Lagom modes run the GEMMs on
+    // num_sms - max NC so the collective's CTAs never queue behind them.
+    int sm_target = 0;
+    if (opts.reserve_comm_sms && cfgs && (mode == Mode::Lagom || mode == Mode::LagomE2E)) {
+      int nc = 0;
+      for (const CommConfig& c : *cfgs) nc = std::max(nc, c.num_channels);
+      sm_target = std::max(1, num_sms - nc);
+    }
     const bool do_comm = mode != Mode::ComputeOnly;
     const std::size_t M = dag.compute_ops.size(), N = comms.size();
     coord.barrier();
@@ -417,10 +472,18 @@ struct ReplayEngine::Impl {
     if (e2e && host_in)
       cuda_check(cudaMemcpyAsync(gemms[0][0].A, host_in, opts.e2e_in_bytes, cudaMemcpyHostToDevice, cs), "h2d");
     cuda_check(cudaStreamWaitEvent(ks, ev_start, 0), "wait");
+    const bool spans_on = do_comm && spans && mode != Mode::Nccl;
+    if (spans_on) {
+      // {start, end} pairs: start <- UINT64_MAX, end <- 0
+      cuda_check(cudaMemset2DAsync(spans, 2 * sizeof(unsigned long long), 0xff, sizeof(unsigned long long), N, ks),
+                 "span init");
+      cuda_check(cudaMemset2DAsync(spans + 1, 2 * sizeof(unsigned long long), 0, sizeof(unsigned long long), N, ks),
+                 "span init");
+    }
     if (do_compute) {
       for (std::size_t i = 0; i < M; ++i) {
         cuda_check(cudaEventRecord(ev_cb[i], cs), "record");
-        for (const Gemm& g : gemms[i]) launch_gemm(g);
+        for (Gemm& g : gemms[i]) launch_gemm(g, sm_target);
         cuda_check(cudaEventRecord(ev_ce[i], cs), "record");
       }
     }
@@ -429,7 +492,7 @@ struct ReplayEngine::Impl {
         if (do_compute && comms[j].dep >= 0) cuda_check(cudaStreamWaitEvent(ks, ev_ce[comms[j].dep], 0), "wait");
         cuda_check(cudaEventRecord(ev_kb[j], ks), "record");
         if (mode == Mode::Nccl) launch_comm_nccl(comms[j]);
-        else launch_comm_lagom(comms[j], (*cfgs)[j]);
+        else launch_comm_lagom(comms[j], (*cfgs)[j], spans ? spans + 2 * j : nullptr);
         cuda_check(cudaEventRecord(ev_ke[j], ks), "record");
       }
     }
@@ -452,6 +515,16 @@ struct ReplayEngine::Impl {
     double z = 0.0;
     if (do_comm)
       for (std::size_t j = 0; j < N; ++j) out[j] = us(ev_kb[j], ev_ke[j]);
+    if (spans_on) {
+      // x_j = the kernel's active span (first CTA start .. last CTA end):
+      // excludes time the launch sat queued behind persistent GEMM CTAs.
+      cuda_check(cudaMemcpy(spans_host.data(), spans, 2 * N * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+                 "spans");
+      for (std::size_t j = 0; j < N; ++j) {
+        const unsigned long long a = spans_host[2 * j], b = spans_host[2 * j + 1];
+        if (b >= a && a != ~0ull) out[j] = static_cast<double>(b - a) * 1e-3;
+      }
+    }
     if (do_compute)
       for (std::size_t i = 0; i < M; ++i) out[N + i] = us(ev_cb[i], ev_ce[i]);
     z = std::max(us(ev_start, ev_cend), us(ev_start, ev_kend));

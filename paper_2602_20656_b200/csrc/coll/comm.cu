@@ -162,6 +162,7 @@ KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
   p.off_slots = c->off_slots;
   p.abort_flag = c->abort_dev;
   p.timeout_ns = static_cast<uint64_t>(c->opts.timeout_ms) * 1000000ull;
+  p.span = static_cast<unsigned long long*>(a->span_out);
   return p;
 }
 

@@ -52,6 +52,7 @@ struct KParams {
   int64_t off_ready, off_freed, off_sstep, off_rstep, off_slots;
   unsigned int* abort_flag;  // host-mapped, sticky
   uint64_t timeout_ns;
+  unsigned long long* span;  // optional {min start, max end} in globaltimer ns
 };
 
 // --------------------------------------------------------- memory model ----
@@ -735,6 +736,7 @@ template <int KIND, int PROTO, class R>
 __global__ void __launch_bounds__(640) coll_kernel(const __grid_constant__ KParams P) {
   __shared__ int s_abort[2];
   if (threadIdx.x < 2) s_abort[threadIdx.x] = 0;
+  if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
   __syncthreads();
   const int r = P.rank < 0 ? static_cast<int>(blockIdx.y) : P.rank;
   const int ch = blockIdx.x, nch = gridDim.x;
@@ -744,6 +746,10 @@ __global__ void __launch_bounds__(640) coll_kernel(const __grid_constant__ KPara
   else if constexpr (KIND == kRingAR) ring_allreduce<PROTO, R>(all, P, r, ch, nch);
   else if constexpr (KIND == kTreeAR) tree_allreduce<PROTO, R>(P, r, ch, nch, s_abort);
   else alltoall<PROTO>(all, P, r, ch, nch);
+  if (P.span) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+  }
 }
 
 }  // namespace lagom_dev
