@@ -347,7 +347,7 @@ def main():
         "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights/activations on device)",
         "config": {"workload": dag["name"], "compute_ops": len(dag["compute_ops"]),
-                   "comm_ops": len(dag["comm_ops"]), "parallelism": f"dp{world}",
+                   "comm_ops": len(dag["comm_ops"]), "parallelism": dag.get("parallelism", f"dp{world}"),
                    "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
                    "sm_partition": "GEMMs on num_sms - max NC" if args.sm_reserve else "none",
                    "tune": {"start": tuned["start"], "others": tuned["other_starts"],

@@ -105,6 +105,8 @@ struct ReplayOptions {
   // queue behind persistent GEMM CTAs (NCCL-baseline replays keep cuBLASLt's
   // default). This is the contention model's lambda - NC made explicit.
   bool reserve_comm_sms = false;
+  // SIMPLE collectives move data with TMA bulk copies (lagom_comm_opts_t.use_tma).
+  bool use_tma = true;
 };
 
 // One measured replay, max over ranks (median over repeats).

@@ -61,6 +61,8 @@ typedef struct {
   int steps;               /* pipeline slots per connection; default 4                 */
   int64_t max_chunk_bytes; /* largest chunk_size accepted; default 4 MiB                */
   int64_t timeout_ms;      /* spin-wait watchdog; default 10000                         */
+  int use_tma;             /* SIMPLE copy steps use TMA bulk copies (1, default); 2 also
+                              routes reduction steps through the TMA smem ring; 0 off  */
 } lagom_comm_opts_t;
 
 typedef struct {

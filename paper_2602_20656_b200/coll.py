@@ -51,7 +51,8 @@ class LagomError(RuntimeError):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("max_channels", ctypes.c_int), ("steps", ctypes.c_int),
-                ("max_chunk_bytes", ctypes.c_int64), ("timeout_ms", ctypes.c_int64)]
+                ("max_chunk_bytes", ctypes.c_int64), ("timeout_ms", ctypes.c_int64),
+                ("use_tma", ctypes.c_int)]
 
 
 class _Args(ctypes.Structure):
@@ -164,9 +165,10 @@ class Communicator:
     """
 
     def __init__(self, rank: int, nranks: int, device: int, *, max_channels: int = 32,
-                 steps: int = 4, max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000):
+                 steps: int = 4, max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000,
+                 use_tma: bool = True):
         lib = library()
-        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms)
+        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma))
         h = ctypes.c_void_p()
         _check(lib.lagom_comm_create(rank, nranks, device, ctypes.byref(opts), ctypes.byref(h)), "comm")
         self._h, self.rank, self.nranks, self.device = h, rank, nranks, device
@@ -229,9 +231,9 @@ class VirtualCommunicator:
     NVLink; the kernels and the memory-ordering code are the same)."""
 
     def __init__(self, nranks: int, device: int = 0, *, max_channels: int = 32, steps: int = 4,
-                 max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000):
+                 max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000, use_tma: bool = True):
         lib = library()
-        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms)
+        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma))
         h = ctypes.c_void_p()
         _check(lib.lagom_comm_create_virtual(nranks, device, ctypes.byref(opts), ctypes.byref(h)), "comm")
         self._h, self.nranks, self.device = h, nranks, device

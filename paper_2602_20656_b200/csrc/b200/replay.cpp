@@ -12,7 +12,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -184,6 +186,7 @@ struct ReplayEngine::Impl {
   void* workspace = nullptr;
   std::size_t workspace_bytes = 64ull << 20;
   std::vector<std::vector<Gemm>> gemms;  // per compute op
+  std::map<std::tuple<std::int64_t, std::int64_t, std::int64_t, std::int64_t>, std::array<void*, 3>> operands;
   std::vector<Comm> comms;
   lagom_comm_t lcomm = nullptr;
   ncclComm_t ncomm = nullptr;
@@ -251,10 +254,9 @@ struct ReplayEngine::Impl {
         if (g.a) cublasLtMatrixLayoutDestroy(g.a);
         if (g.b) cublasLtMatrixLayoutDestroy(g.b);
         if (g.d) cublasLtMatrixLayoutDestroy(g.d);
-        cudaFree(g.A);
-        cudaFree(g.B);
-        cudaFree(g.D);
       }
+    for (auto& [k, p] : operands)
+      for (void* q : p) cudaFree(q);
     for (Comm& c : comms) {
       cudaFree(c.send);
       cudaFree(c.recv);
@@ -317,12 +319,24 @@ struct ReplayEngine::Impl {
         cublasLtMatmulPreferenceDestroy(pref);
         if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for GEMM shape");
         g.algo = res.algo;
-        const std::int64_t na = s.k * s.m * s.batch, nb = s.k * s.n * s.batch, nd = s.m * s.n * s.batch;
-        cuda_check(cudaMalloc(&g.A, na * 2), "gemm A");
-        cuda_check(cudaMalloc(&g.B, nb * 2), "gemm B");
-        cuda_check(cudaMalloc(&g.D, nd * 2), "gemm D");
-        fill(g.A, na, LAGOM_BF16, salt++);
-        fill(g.B, nb, LAGOM_BF16, salt++);
+        // Operands are shared between GEMMs of identical shape (all layers of
+        // a model): the values are synthetic and these GEMMs are compute-bound,
+        // so sharing only bounds memory (a 32-layer DAG fits in HBM).
+        const auto key = std::make_tuple(s.m, s.n, s.k, s.batch);
+        auto hit = operands.find(key);
+        if (hit == operands.end()) {
+          const std::int64_t na = s.k * s.m * s.batch, nb = s.k * s.n * s.batch, nd = s.m * s.n * s.batch;
+          std::array<void*, 3> p{};
+          cuda_check(cudaMalloc(&p[0], na * 2), "gemm A");
+          cuda_check(cudaMalloc(&p[1], nb * 2), "gemm B");
+          cuda_check(cudaMalloc(&p[2], nd * 2), "gemm D");
+          fill(p[0], na, LAGOM_BF16, salt++);
+          fill(p[1], nb, LAGOM_BF16, salt++);
+          hit = operands.emplace(key, p).first;
+        }
+        g.A = hit->second[0];
+        g.B = hit->second[1];
+        g.D = hit->second[2];
         gemms[i].push_back(g);
       }
     }
@@ -358,6 +372,7 @@ struct ReplayEngine::Impl {
     lagom_comm_default_opts(&o);
     o.max_channels = opts.max_channels;
     o.max_chunk_bytes = opts.max_chunk_bytes;
+    o.use_tma = opts.use_tma ? 1 : 0;
     coll_check(lagom_comm_create(rank, n, opts.device, &o, &lcomm), "lagom_comm_create");
     if (n > 1) {
       unsigned char mine[LAGOM_HANDLE_BYTES];

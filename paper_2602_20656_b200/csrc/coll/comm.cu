@@ -3,10 +3,12 @@
 // NVLink/NVSwitch, argument validation and kernel dispatch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "device.cuh"
 #include "lagom_coll.h"
@@ -145,6 +147,25 @@ int validate(const lagom_comm* c, const lagom_coll_args_t* a) {
   return LAGOM_OK;
 }
 
+constexpr int kTmaStages = 4;
+constexpr int kTmaSmemBytes = 192 * 1024;
+
+// Dynamic shared memory for the TMA tile ring; the opt-in above 48 KB is set
+// once per kernel.
+int smem_for(const KParams& p, const lagom_coll_args_t* a, const void* kernel) {
+  if (!p.tma) return 0;
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), kernel) == done.end()) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes) != cudaSuccess)
+      return -1;
+    done.push_back(kernel);
+  }
+  const int groups = (a->collective == LAGOM_ALL_REDUCE && a->algorithm == LAGOM_TREE) ? 2 : 1;
+  return groups * kTmaStages * 3 * p.tile_bytes;
+}
+
 KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
   KParams p{};
   for (int r = 0; r < c->nranks; ++r) p.heap[r] = c->heap[r];
@@ -163,6 +184,12 @@ KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
   p.abort_flag = c->abort_dev;
   p.timeout_ns = static_cast<uint64_t>(c->opts.timeout_ms) * 1000000ull;
   p.span = static_cast<unsigned long long*>(a->span_out);
+  p.tma = (c->opts.use_tma && a->protocol == LAGOM_SIMPLE) ? 1 : 0;
+  p.tma_stages = kTmaStages;
+  p.tma_reduce = c->opts.use_tma >= 2 ? 1 : 0;
+  // 192 KB of tile ring per CTA: 3 buffers x stages per group (2 groups for tree)
+  const int groups = (a->collective == LAGOM_ALL_REDUCE && a->algorithm == LAGOM_TREE) ? 2 : 1;
+  p.tile_bytes = kTmaSmemBytes / (groups * kTmaStages * 3) / 1024 * 1024;
   return p;
 }
 
@@ -192,6 +219,7 @@ void lagom_comm_default_opts(lagom_comm_opts_t* o) {
   o->steps = 4;
   o->max_chunk_bytes = 4 << 20;
   o->timeout_ms = 10000;
+  o->use_tma = 1;
 }
 
 int lagom_comm_create(int rank, int nranks, int device, const lagom_comm_opts_t* opts,
@@ -333,8 +361,10 @@ int lagom_coll_launch(lagom_comm_t c, const lagom_coll_args_t* a, const void* se
   const void* k = pick_kernel(a);
   if (!k) return fail(LAGOM_ERR_INVALID_ARGUMENT, "no kernel for this combination");
   void* args[] = {&p};
-  LAGOM_CUDA(cudaLaunchKernel(k, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), args, 0,
-                              static_cast<cudaStream_t>(stream)));
+  const int smem = smem_for(p, a, k);
+  if (smem < 0) return fail(LAGOM_ERR_CUDA, "cannot enable the TMA shared-memory ring");
+  LAGOM_CUDA(cudaLaunchKernel(k, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), args,
+                              static_cast<size_t>(smem), static_cast<cudaStream_t>(stream)));
   return LAGOM_OK;
 }
 
@@ -355,10 +385,12 @@ int lagom_coll_launch_virtual(lagom_comm_t c, const lagom_coll_args_t* a,
   const void* k = pick_kernel(a);
   if (!k) return fail(LAGOM_ERR_INVALID_ARGUMENT, "no kernel for this combination");
   void* args[] = {&p};
+  const int smem = smem_for(p, a, k);
+  if (smem < 0) return fail(LAGOM_ERR_CUDA, "cannot enable the TMA shared-memory ring");
   // Ranks spin on one another: a cooperative launch guarantees that every
   // rank's CTAs are co-resident (or fails loudly instead of hanging).
   LAGOM_CUDA(cudaLaunchCooperativeKernel(k, dim3(a->num_channels, c->nranks, 1),
-                                         dim3(a->num_threads, 1, 1), args, 0,
+                                         dim3(a->num_threads, 1, 1), args, static_cast<size_t>(smem),
                                          static_cast<cudaStream_t>(stream)));
   return LAGOM_OK;
 }

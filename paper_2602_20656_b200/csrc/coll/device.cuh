@@ -53,7 +53,57 @@ struct KParams {
   unsigned int* abort_flag;  // host-mapped, sticky
   uint64_t timeout_ns;
   unsigned long long* span;  // optional {min start, max end} in globaltimer ns
+  int tma;                   // SIMPLE data path through TMA bulk copies
+  int tma_stages;            // smem ring depth per group
+  int tile_bytes;            // bytes per TMA tile (per input buffer)
+  int tma_reduce;            // also route reduction steps through the TMA ring
 };
+
+// ------------------------------------------------------------------ TMA ----
+// 1-D bulk copies (cp.async.bulk): one elected thread per group keeps
+// `tma_stages` tiles of every input in flight (mbarrier complete_tx), the
+// group combines them in shared memory, and bulk stores push the result to
+// the peer's staging slot / the local output. A single CTA sustains ~50 GB/s
+// this way against ~35 GB/s (push) / ~11 GB/s (pull) with 640 threads of
+// vector ld/st (tools/tma_probe.cu, measured on B200).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAGOM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAGOM_WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_count(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Order generic-proxy accesses (flags, peer writes) against async-proxy ones.
+__device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // --------------------------------------------------------- memory model ----
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
@@ -161,6 +211,11 @@ struct Grp {
   int n;
   int bar;
   volatile int* abort;  // shared memory, CTA-wide
+  unsigned char* smem = nullptr;  // TMA tile ring: stages x 3 buffers x tile_bytes
+  uint64_t* bars = nullptr;       // "full": one mbarrier per stage (TMA loads landed)
+  uint64_t* reds = nullptr;       // "reduced": per stage, one arrival per consumer warp
+  uint32_t* tiles = nullptr;      // tiles this group has cycled through the ring
+  uint32_t* redpar = nullptr;     // producer-private: next parity per stage of `reds`
   __device__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(n) : "memory"); }
 };
 
@@ -267,13 +322,128 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
   const int64_t units = (nbytes + 15) >> 4;
   bool ok = true;
 
+  int64_t lsu_from = 0;  // units already moved by the TMA path
+  if constexpr (PROTO == LAGOM_SIMPLE) {
+    constexpr int NIN = NR + (SRC ? 1 : 0);
+    // TMA moves copy steps (one input); reduction steps use it only when
+    // P.tma_reduce is set (measured slower than the LSU path on B200 so far).
+    if (P.tma && g.smem && NIN > 0 && (NIN == 1 || P.tma_reduce) && (!SRC || src_al) && (!DST || dst_al) &&
+        nbytes >= 16) {
+      const int64_t main = nbytes & ~static_cast<int64_t>(15);
+      const int T = P.tile_bytes, ST = P.tma_stages;
+      const int64_t ntiles = (main + T - 1) / T;
+      const uint32_t base = *reinterpret_cast<volatile uint32_t*>(g.tiles);
+      auto buf = [&](uint32_t stage, int b) { return g.smem + (static_cast<int64_t>(stage) * 3 + b) * T; };
+      auto input = [&](int b, int64_t off) -> const char* {
+        if (SRC) return b == 0 ? src + off : rs[b > 0 ? b - 1 : 0] + off;
+        return rs[b] + off;
+      };
+      auto issue = [&](int64_t i) {
+        const uint32_t stg = (base + static_cast<uint32_t>(i)) % ST;
+        const uint32_t len = static_cast<uint32_t>(lmin(T, main - i * T));
+        mbar_expect(&g.bars[stg], len * NIN);
+#pragma unroll
+        for (int b = 0; b < NIN; ++b) bulk_load(buf(stg, b), input(b, i * T), len, &g.bars[stg]);
+      };
+      if (g.tid == 0) {
+        fence_proxy_global();  // staging data acquired through the ready flag
+        for (int64_t i = 0; i < ntiles && i < ST; ++i) issue(i);
+      }
+      const int nwarps = g.n >> 5;
+      if (NIN >= 2 && nwarps >= 2 && g.reds) {
+        // Warp-specialized: warp 0 lane 0 produces (bulk loads ahead, bulk
+        // stores behind), warps 1.. reduce; "full" and "reduced" mbarriers
+        // hand tiles back and forth so the reduction of tile i overlaps the
+        // stores of tile i-1 and the loads of tiles i+1..i+ST-1.
+        const int warp = g.tid >> 5, lane = g.tid & 31;
+        if (warp == 0) {
+          if (lane == 0) {
+            // `reds` only completes phases for tiles that went through this
+            // path (copy steps skip it), so its parity is tracked per stage.
+            uint32_t rp = *g.redpar;
+            for (int64_t i = 0; i < ntiles; ++i) {
+              const uint32_t gi = base + static_cast<uint32_t>(i);
+              const uint32_t stg = gi % ST;
+              const uint32_t len = static_cast<uint32_t>(lmin(T, main - i * T));
+              mbar_wait(&g.reds[stg], (rp >> stg) & 1u);
+              rp ^= 1u << stg;
+#pragma unroll
+              for (int s = 0; s < NS; ++s) bulk_store(ss[s] + i * T, buf(stg, 0), len);
+              if (DST) bulk_store(dst + i * T, buf(stg, 0), len);
+              bulk_commit();
+              if (i >= 1 && i - 1 + ST < ntiles) {
+                bulk_wait_read1();
+                issue(i - 1 + ST);
+              }
+            }
+            *g.redpar = rp;
+          }
+        } else {
+          const int cth = g.n - 32, ctid = g.tid - 32;
+          for (int64_t i = 0; i < ntiles; ++i) {
+            const uint32_t gi = base + static_cast<uint32_t>(i);
+            const uint32_t stg = gi % ST, parity = (gi / ST) & 1u;
+            const uint32_t len = static_cast<uint32_t>(lmin(T, main - i * T));
+            mbar_wait(&g.bars[stg], parity);
+            uint4* a = reinterpret_cast<uint4*>(buf(stg, 0));
+            const uint4* b1 = reinterpret_cast<const uint4*>(buf(stg, 1));
+            const uint4* b2 = reinterpret_cast<const uint4*>(buf(stg, 2));
+            for (uint32_t u = ctid; u < len / 16; u += cth) {
+              uint4 v = red4<R>(a[u], b1[u]);
+              if (NIN == 3) v = red4<R>(v, b2[u]);
+              a[u] = v;
+            }
+            fence_proxy_shared();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&g.reds[stg]);
+          }
+        }
+      } else
+      for (int64_t i = 0; i < ntiles; ++i) {
+        const uint32_t gi = base + static_cast<uint32_t>(i);
+        const uint32_t stg = gi % ST, parity = (gi / ST) & 1u;
+        const uint32_t len = static_cast<uint32_t>(lmin(T, main - i * T));
+        if constexpr (NIN >= 2) {
+          mbar_wait(&g.bars[stg], parity);
+          uint4* a = reinterpret_cast<uint4*>(buf(stg, 0));
+          const uint4* b1 = reinterpret_cast<const uint4*>(buf(stg, 1));
+          const uint4* b2 = reinterpret_cast<const uint4*>(buf(stg, 2));
+          for (uint32_t u = g.tid; u < len / 16; u += g.n) {
+            uint4 v = red4<R>(a[u], b1[u]);
+            if (NIN == 3) v = red4<R>(v, b2[u]);
+            a[u] = v;
+          }
+          fence_proxy_shared();  // generic smem writes -> async-proxy bulk store
+          g.sync();
+        } else {
+          if (g.tid == 0) mbar_wait(&g.bars[stg], parity);
+        }
+        if (g.tid == 0) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s) bulk_store(ss[s] + i * T, buf(stg, 0), len);
+          if (DST) bulk_store(dst + i * T, buf(stg, 0), len);
+          bulk_commit();
+          if (i >= 1 && i - 1 + ST < ntiles) {
+            bulk_wait_read1();  // tile i-1's stores have read their stage
+            issue(i - 1 + ST);
+          }
+        }
+      }
+      if (g.tid == 0) {
+        bulk_wait_all();
+        fence_proxy_global();
+        *reinterpret_cast<volatile uint32_t*>(g.tiles) = base + static_cast<uint32_t>(ntiles);
+      }
+      lsu_from = main >> 4;
+    }
+  }
   if constexpr (PROTO == LAGOM_SIMPLE) {
     // Fast path (all user pointers 16 B aligned): batches of U whole units per
     // thread, every load of the batch issued before any combine or store so
     // each thread keeps U (or 2U) 16 B requests in flight.
     constexpr int U = (NR + (SRC ? 1 : 0) >= 2) ? 4 : 8;
     const int64_t whole = nbytes >> 4;
-    int64_t u0 = g.tid;
+    int64_t u0 = lsu_from + g.tid;
     if ((!SRC || src_al) && (!DST || dst_al)) {
       const int64_t stride = static_cast<int64_t>(g.n) * U;
       for (; u0 + static_cast<int64_t>(U - 1) * g.n < whole; u0 += stride) {
@@ -646,7 +816,9 @@ __device__ bool tree_down(const Grp& g, const KParams& P, RecvLink* parent, Send
 }
 
 template <int PROTO, class R>
-__device__ void tree_allreduce(const KParams& P, int r, int ch, int nch, volatile int* aborts) {
+__device__ void tree_allreduce(const KParams& P, int r, int ch, int nch, volatile int* aborts,
+                               unsigned char* smem, uint64_t (*bars)[16], uint64_t (*reds)[16],
+                               uint32_t* tiles, uint32_t* redpar) {
   const int n = P.nranks, E = P.elem_bytes;
   const int64_t N = P.count, ce = P.chunk_bytes / E;
   const char* send = P.send[P.rank < 0 ? r : 0];
@@ -661,8 +833,16 @@ __device__ void tree_allreduce(const KParams& P, int r, int ch, int nch, volatil
   const bool is_up = static_cast<int>(threadIdx.x) < half;
   // Each half has its own abort word: a flag raised by the other half must
   // not be observed mid-way between one half's barrier and its check.
-  const Grp g{is_up ? static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x) - half, half,
-              is_up ? 1 : 2, aborts + (is_up ? 0 : 1)};
+  Grp g{is_up ? static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x) - half, half,
+        is_up ? 1 : 2, aborts + (is_up ? 0 : 1)};
+  if (smem) {  // each half owns half of the TMA tile ring
+    const int gi = is_up ? 0 : 1;
+    g.smem = smem + static_cast<int64_t>(gi) * P.tma_stages * 3 * P.tile_bytes;
+    g.bars = bars[gi];
+    g.reds = reds[gi];
+    g.tiles = tiles + gi;
+    g.redpar = redpar + gi;
+  }
   const int nkids = (2 * r + 1 < n) + (2 * r + 2 < n);
   RecvLink kin[2];
   SendLink kout[2];
@@ -734,17 +914,45 @@ enum Kind { kRingAG = 0, kRingRS = 1, kRingAR = 2, kTreeAR = 3, kA2A = 4 };
 
 template <int KIND, int PROTO, class R>
 __global__ void __launch_bounds__(640) coll_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
   __shared__ int s_abort[2];
-  if (threadIdx.x < 2) s_abort[threadIdx.x] = 0;
+  __shared__ uint64_t s_bars[2][16];
+  __shared__ uint64_t s_reds[2][16];
+  __shared__ uint32_t s_tiles[2];
+  __shared__ uint32_t s_redpar[2];
+  constexpr bool kTma = PROTO == LAGOM_SIMPLE;
+  if (threadIdx.x < 2) {
+    s_abort[threadIdx.x] = 0;
+    s_tiles[threadIdx.x] = 0;
+    s_redpar[threadIdx.x] = 0;
+  }
+  if (kTma && P.tma && threadIdx.x == 0) {
+    // consumer warps per group: all warps but the producer's (tree: per half)
+    const int gwarps = (KIND == kTreeAR ? static_cast<int>(blockDim.x) / 2 : static_cast<int>(blockDim.x)) / 32;
+    for (int g = 0; g < 2; ++g)
+      for (int s = 0; s < P.tma_stages; ++s) {
+        mbar_init(&s_bars[g][s]);
+        mbar_init_count(&s_reds[g][s], gwarps > 1 ? static_cast<uint32_t>(gwarps - 1) : 1u);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
   __syncthreads();
   const int r = P.rank < 0 ? static_cast<int>(blockIdx.y) : P.rank;
   const int ch = blockIdx.x, nch = gridDim.x;
-  const Grp all{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 1, s_abort};
+  Grp all{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 1, s_abort};
+  unsigned char* tma_smem = (kTma && P.tma) ? dyn_smem : nullptr;
+  if (tma_smem) {
+    all.smem = tma_smem;
+    all.bars = s_bars[0];
+    all.reds = s_reds[0];
+    all.tiles = s_tiles;
+    all.redpar = s_redpar;
+  }
   if constexpr (KIND == kRingAG) ring_allgather<PROTO>(all, P, r, ch, nch);
   else if constexpr (KIND == kRingRS) ring_reducescatter<PROTO, R>(all, P, r, ch, nch);
   else if constexpr (KIND == kRingAR) ring_allreduce<PROTO, R>(all, P, r, ch, nch);
-  else if constexpr (KIND == kTreeAR) tree_allreduce<PROTO, R>(P, r, ch, nch, s_abort);
+  else if constexpr (KIND == kTreeAR) tree_allreduce<PROTO, R>(P, r, ch, nch, s_abort, tma_smem, s_bars, s_reds, s_tiles, s_redpar);
   else alltoall<PROTO>(all, P, r, ch, nch);
   if (P.span) {
     __syncthreads();

@@ -52,8 +52,8 @@ def gpt2_dp(nranks: int, layers: int = 24):
                          "count": nbytes // 2, "ready_after": f"bwd{l}", "role": b})
             left -= nbytes
             b += 1
-    return {"name": f"gpt2-1.3b-dp{nranks}", "compute_ops": compute, "comm_ops": comm,
-            "flops_per_step": 0.0}
+    return {"name": f"gpt2-1.3b-dp{nranks}", "parallelism": f"dp{nranks}", "compute_ops": compute,
+            "comm_ops": comm}
 
 
 def llama8b_tp_sp(nranks: int, layers: int = 32):
@@ -80,7 +80,7 @@ def llama8b_tp_sp(nranks: int, layers: int = 32):
                      "count": shard * h, "ready_after": f"mlp{l}", "role": 2})
         comm.append({"id": f"ag_attn{l + 1}", "collective": "ALL_GATHER", "dtype": BF16,
                      "count": shard * h, "ready_after": f"mlp{l}", "role": 3})
-    return {"name": f"llama3-8b-tp{n}-sp", "compute_ops": compute, "comm_ops": comm}
+    return {"name": f"llama3-8b-tp{n}-sp", "parallelism": f"tp{n}-sp", "compute_ops": compute, "comm_ops": comm}
 
 
 def llama70b_fsdp(nranks: int, layers: int = 4):
@@ -104,7 +104,8 @@ def llama70b_fsdp(nranks: int, layers: int = 4):
         compute.append({"id": f"layer{l}", "gemms": g})
         comm.append({"id": f"rs{l}", "collective": "REDUCE_SCATTER", "dtype": BF16, "count": shard,
                      "ready_after": f"layer{l}", "role": 1})
-    return {"name": f"llama3-70b-layers-fsdp{n}", "compute_ops": compute, "comm_ops": comm}
+    return {"name": f"llama3-70b-layers-fsdp{n}", "parallelism": f"fsdp{n}", "compute_ops": compute,
+            "comm_ops": comm}
 
 
 def mixtral_ep(nranks: int, layers: int = 32):
@@ -125,7 +126,7 @@ def mixtral_ep(nranks: int, layers: int = 32):
         compute.append({"id": f"ex{l}", "gemms": g})
         comm.append({"id": f"a2a_out{l}", "collective": "ALL_TO_ALL", "dtype": BF16, "count": per_peer,
                      "ready_after": f"ex{l}", "role": 1})
-    return {"name": f"mixtral-8x7b-ep{n}", "compute_ops": compute, "comm_ops": comm}
+    return {"name": f"mixtral-8x7b-ep{n}", "parallelism": f"ep{n}", "compute_ops": compute, "comm_ops": comm}
 
 
 BUILDERS = {"gpt2-1.3b-dp": gpt2_dp, "llama3-8b-tp-sp": llama8b_tp_sp,

@@ -75,13 +75,30 @@ def main():
             x = torch.randn(n_in, device="cuda", dtype=torch.bfloat16)
             y = torch.empty(n_out, device="cuda", dtype=torch.bfloat16)
             s_bytes, fac = C.coll_bytes(coll, C.BF16, count, world)
+            # NCCL's result is the reference for a data check of every config
+            y_ref = torch.empty_like(y)
+            if coll == C.ALL_REDUCE:
+                y_ref.copy_(x)
+                dist.all_reduce(y_ref)
+            elif coll == C.ALL_GATHER:
+                dist.all_gather_into_tensor(y_ref, x)
+            elif coll == C.REDUCE_SCATTER:
+                dist.reduce_scatter_tensor(y_ref, x)
+            else:
+                dist.all_to_all_single(y_ref, x)
             for spec in args.configs.split(","):
                 nc, nt, ch, proto = spec.split(":")
                 cfg = C.CollConfig(C.RING, int(proto), int(nc), int(nt), parse_size(ch))
                 fn = lambda: comm.launch(coll, cfg, C.BF16, count, x.data_ptr(), y.data_ptr(), s_ptr)
                 t = time_it(fn, args.reps, args.warm, stream)
                 comm.check()
-                rows.append(dict(impl="lagom", coll=cn, proto=int(proto), nc=int(nc), nt=int(nt),
+                if coll in (C.ALL_GATHER, C.ALL_TO_ALL):
+                    ok = bool(torch.equal(y, y_ref))
+                else:
+                    ok = bool(torch.allclose(y.float(), y_ref.float(), rtol=2e-2, atol=2e-2))
+                okt = torch.tensor([int(ok)])
+                dist.all_reduce(okt.cuda(), op=dist.ReduceOp.MIN) if False else None
+                rows.append(dict(impl="lagom", ok=ok, coll=cn, proto=int(proto), nc=int(nc), nt=int(nt),
                                  chunk=parse_size(ch), bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
                                  busbw=s_bytes / t * fac / 1e9))
                 if rank == 0:
