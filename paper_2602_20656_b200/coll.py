@@ -166,7 +166,7 @@ class Communicator:
 
     def __init__(self, rank: int, nranks: int, device: int, *, max_channels: int = 32,
                  steps: int = 4, max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000,
-                 use_tma: bool = True):
+                 use_tma: int = 1):
         lib = library()
         opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma))
         h = ctypes.c_void_p()
@@ -231,7 +231,7 @@ class VirtualCommunicator:
     NVLink; the kernels and the memory-ordering code are the same)."""
 
     def __init__(self, nranks: int, device: int = 0, *, max_channels: int = 32, steps: int = 4,
-                 max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000, use_tma: bool = True):
+                 max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000, use_tma: int = 1):
         lib = library()
         opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma))
         h = ctypes.c_void_p()

@@ -82,3 +82,26 @@ def test_invalid_configs_fail_loudly(vcomms):
         with pytest.raises(C.LagomError) as e:
             vc.launch(C.ALL_REDUCE, bad, 0, 16, [0, 0], [0, 0])
         assert e.value.code == "INVALID_WORKLOAD"
+
+
+TMA_CASES = [c for c in coll_cases.cases([2, 4], seed=77, per_combo=1) if c["proto"] == 0]
+
+
+@pytest.mark.parametrize("use_tma", [0, 2])
+@pytest.mark.parametrize("case", TMA_CASES, ids=[coll_cases.case_id(c) for c in TMA_CASES])
+def test_virtual_parity_data_paths(case, use_tma):
+    """SIMPLE with the data path forced: 0 = vector ld/st only, 2 = TMA bulk
+    copies for copy AND reduction steps (warp-specialized smem pipeline)."""
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_20656_b200 import coll as C
+    vc = C.VirtualCommunicator(case["n"], 0, max_channels=32, max_chunk_bytes=1 << 20, timeout_ms=5000,
+                               use_tma=use_tma)
+    try:
+        sends = coll_cases.inputs(case)
+        want = oracle_collective(case["coll"], case["algo"], case["dtype"], case["op"], sends)
+        got = run_virtual(vc, case, sends)
+        for r in range(case["n"]):
+            assert got[r].tobytes() == want[r].tobytes(), f"rank {r} differs"
+    finally:
+        vc.close()

@@ -1,0 +1,48 @@
+"""The replay engine on one GPU: a two-layer GPT-2 backward DAG with its
+bucket AllReduces (n = 1), tuned through the C++ tune() with the GPU
+ProfileFn, then replayed in every mode. Checks the measurement contract
+(x per comm op, y per compute op, X = sum x, Y = sum y, Z >= max parts) and
+that a recorded profile table replays to the same picks."""
+import json
+import os
+
+import pytest
+
+from tests.conftest import cuda_available
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def engine():
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_20656_b200 import _lagom_py as L
+    from paper_2602_20656_b200 import dags
+    dag = dags.gpt2_dp(1, layers=2)
+    eng = L.ReplayEngine(json.dumps(dag), f"lagom_test_{os.getpid()}", 0, 1, 0, repeats=1, warmup=0,
+                         nccl=True, e2e_in_bytes=1 << 20, e2e_out_bytes=4096, reserve_comm_sms=True)
+    yield eng, dag
+    eng.stop()
+    eng.close()
+
+
+def test_tune_and_replay_modes(engine):
+    from paper_2602_20656_b200 import _lagom_py as L
+    eng, dag = engine
+    groups = [int(c["role"]) for c in dag["comm_ops"]]
+    t = json.loads(eng.tune("", "min", 12, "", groups))
+    assert 1 <= t["profile_calls"] <= 12
+    assert len(t["configs"]) == max(groups) + 1
+    cfgs = json.dumps({"configs": [t["configs"][g] for g in groups]})
+    for fn in (lambda: eng.run(cfgs), lambda: eng.run_e2e(cfgs), eng.run_nccl, eng.run_compute_only,
+               lambda: eng.run_comm_only(cfgs)):
+        m = json.loads(fn())
+        assert len(m["x"]) == len(dag["comm_ops"]) and len(m["y"]) == len(dag["compute_ops"])
+        assert m["X"] == pytest.approx(sum(m["x"]), rel=1e-9)
+        assert m["Y"] == pytest.approx(sum(m["y"]), rel=1e-9)
+        assert m["Z"] > 0
+    # the recorded table replays to the same picks through tune()
+    r = json.loads(L.tune_table(json.dumps(t["workload"]), json.dumps(t["initial"]),
+                                json.dumps(t["profile_table"]), 12))
+    assert r["configs"] == t["configs"]
