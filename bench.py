@@ -179,6 +179,11 @@ def main():
     ap.add_argument("--start", default="best", choices=["min", "nccl-default", "best"],
                     help="tune() seed (reference CLI --start); best = run both, keep the lower final Z")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--nc-max", type=int, default=64, help="per-op CommBounds.nc_max for the search")
+    ap.add_argument("--nvls", type=int, default=1, help="comm buffers in an NVLS region (TREE = in-switch)")
+    ap.add_argument("--params", default=os.path.join(ROOT, "profiles", "fitted_params_b200_n4.json"),
+                    help="subspace params fitted on B200 by tools/contention_profile.py (reference JSON "
+                         "schema); '' = the reference's synthetic defaults")
     ap.add_argument("--sm-reserve", type=int, default=1,
                     help="Lagom replays run GEMMs on num_sms - max NC SMs (cuBLASLt SM count target)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -211,7 +216,7 @@ def main():
     gpu_json = json.dumps({"num_sms": n_sms, "peak_mem_bw": peaks["hbm_gbs"] * 1e3,
                            "link_bw": NVLINK_PEER_GBS * 1e3, "comm_bw_cap_fraction": 0.6})
 
-    dag = dags.BUILDERS[args.workload](world)
+    dag = dags.with_nc_max(dags.BUILDERS[args.workload](world), args.nc_max)
     # Comm roles recur in every layer; the last layer's comms are exposed (no
     # compute left to hide them), so they get groups of their own.
     last_compute = dag["compute_ops"][-1]["id"]
@@ -226,7 +231,8 @@ def main():
     T_in_bytes = 8192 * 2048 * 2
     eng = L.ReplayEngine(json.dumps(dag), f"lagom_{token}", rank, world, local, repeats=1, warmup=0,
                          nccl=not args.no_nccl, e2e_in_bytes=T_in_bytes, e2e_out_bytes=4096,
-                         reserve_comm_sms=bool(args.sm_reserve))
+                         reserve_comm_sms=bool(args.sm_reserve), max_channels=max(32, args.nc_max),
+                         nvls=bool(args.nvls))
     result, tuned, tune_wall_s, tune_runs = None, None, 0.0, {}
     if rank != 0:
         eng.serve()
@@ -238,7 +244,11 @@ def main():
         eng.run_compute_only()  # first-touch / clocks settle before the search
         starts = ["min", "nccl-default"] if args.start == "best" else [args.start]
         eng.set_measurement(3, 1)  # each profile call: median of 3 replays after 1 warmup
-        runs = {st: json.loads(eng.tune(gpu_json, st, args.budget, "", groups)) for st in starts}
+        params_doc = open(args.params).read() if args.params and os.path.exists(args.params) else ""
+        if params_doc:
+            pj = json.loads(params_doc)
+            params_doc = json.dumps(pj.get("params", pj))  # accept a profile file or a bare table
+        runs = {st: json.loads(eng.tune(gpu_json, st, args.budget, params_doc, groups)) for st in starts}
         eng.set_measurement(1, 0)
         # The replays are noisy under the 1 kW power cap, so the starts' final
         # assignments are compared head to head (interleaved) before choosing.
@@ -350,6 +360,8 @@ def main():
                    "comm_ops": len(dag["comm_ops"]), "parallelism": dag.get("parallelism", f"dp{world}"),
                    "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
                    "sm_partition": "GEMMs on num_sms - max NC" if args.sm_reserve else "none",
+                   "params": os.path.relpath(args.params, ROOT) if args.params else "reference defaults",
+                   "nvls": bool(args.nvls) and world > 1,
                    "tune": {"start": tuned["start"], "others": tuned["other_starts"],
                             "groups": len(tuned["configs"]),
                             "profile_calls": tuned["profile_calls"], "boundary": tuned["boundary_condition"],

@@ -107,6 +107,9 @@ struct ReplayOptions {
   bool reserve_comm_sms = false;
   // SIMPLE collectives move data with TMA bulk copies (lagom_comm_opts_t.use_tma).
   bool use_tma = true;
+  // NVSwitch multicast: comm buffers live in an NVLS region, so TREE
+  // AllReduce/AllGather/ReduceScatter run reduced/broadcast in the switch.
+  bool nvls = false;
 };
 
 // One measured replay, max over ranks (median over repeats).

@@ -136,6 +136,20 @@ int lagom_coll_launch_virtual(lagom_comm_t comm, const lagom_coll_args_t* args,
 int lagom_coll_bytes(const lagom_coll_args_t* args, int nranks, int64_t* alg_bytes,
                      double* bus_factor);
 
+/* NVLS (NVLink SHARP multicast) on NVSwitch boxes. With a bound region,
+ * TREE AllReduce / AllGather / ReduceScatter (sum) whose buffers live in the
+ * region run reduced/broadcast inside the switch (multimem.ld_reduce /
+ * multimem.st); other launches keep the P2P kernels. Collective set-up:
+ *   rank 0: lagom_comm_nvls_export(bytes, blob)  -> broadcast blob
+ *   all:    lagom_comm_nvls_import(blob); <barrier>; lagom_comm_nvls_bind()
+ * Allocations (same sequence on every rank) have identical offsets. */
+int lagom_comm_nvls_supported(lagom_comm_t comm);
+int lagom_comm_nvls_export(lagom_comm_t comm, int64_t bytes, void* blob /* LAGOM_HANDLE_BYTES */);
+int lagom_comm_nvls_import(lagom_comm_t comm, const void* blob);
+int lagom_comm_nvls_bind(lagom_comm_t comm);
+int lagom_comm_nvls_alloc(lagom_comm_t comm, int64_t bytes, void** ptr);
+int64_t lagom_comm_nvls_bytes(lagom_comm_t comm);
+
 /* Synthetic data: fills `nelems` elements of `dtype` with uniform values in
  * [-scale, scale) (int32: integers in [-2^20, 2^20)) from a counter-based
  * hash of (seed, index) — deterministic and identical on every GPU. */

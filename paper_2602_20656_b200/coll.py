@@ -68,7 +68,9 @@ EXPORTED_SYMBOLS = (
     "lagom_comm_default_opts", "lagom_comm_create", "lagom_comm_export_handle",
     "lagom_comm_import_handles", "lagom_comm_create_virtual", "lagom_comm_destroy",
     "lagom_comm_info", "lagom_comm_heap_bytes", "lagom_comm_check", "lagom_coll_validate",
-    "lagom_coll_launch", "lagom_coll_launch_virtual", "lagom_coll_bytes",
+    "lagom_coll_launch", "lagom_coll_launch_virtual", "lagom_coll_bytes", "lagom_fill_random",
+    "lagom_comm_nvls_supported", "lagom_comm_nvls_export", "lagom_comm_nvls_import",
+    "lagom_comm_nvls_bind", "lagom_comm_nvls_alloc", "lagom_comm_nvls_bytes",
 )
 
 _lib = None
@@ -103,6 +105,13 @@ def library() -> ctypes.CDLL:
                                               ctypes.POINTER(vp), vp]),
         "lagom_coll_bytes": (c_int, [ctypes.POINTER(_Args), c_int, ctypes.POINTER(c_i64),
                                      ctypes.POINTER(ctypes.c_double)]),
+        "lagom_fill_random": (c_int, [vp, c_i64, c_int, ctypes.c_uint64, ctypes.c_float, vp]),
+        "lagom_comm_nvls_supported": (c_int, [vp]),
+        "lagom_comm_nvls_export": (c_int, [vp, c_i64, ctypes.c_char_p]),
+        "lagom_comm_nvls_import": (c_int, [vp, ctypes.c_char_p]),
+        "lagom_comm_nvls_bind": (c_int, [vp]),
+        "lagom_comm_nvls_alloc": (c_int, [vp, c_i64, ctypes.POINTER(vp)]),
+        "lagom_comm_nvls_bytes": (c_i64, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -195,6 +204,49 @@ class Communicator:
         dist.all_gather_object(handles, comm.export_handle(), group=group)
         comm.import_handles(handles)
         return comm
+
+    # ----------------------------------------------------------------- NVLS
+    def nvls_supported(self) -> bool:
+        return bool(library().lagom_comm_nvls_supported(self._h))
+
+    def enable_nvls(self, nbytes: int, group=None) -> None:
+        """Collective: binds an NVLS multicast region of >= nbytes on every
+        rank (rank 0 creates, peers import, barrier, all bind)."""
+        import torch.distributed as dist
+        lib = library()
+        blob = ctypes.create_string_buffer(HANDLE_BYTES)
+        _check(lib.lagom_comm_nvls_export(self._h, nbytes, blob), "nvls")
+        box = [blob.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        _check(lib.lagom_comm_nvls_import(self._h, box[0]), "nvls")
+        dist.barrier(group=group)
+        _check(lib.lagom_comm_nvls_bind(self._h), "nvls")
+        dist.barrier(group=group)
+
+    def nvls_alloc(self, nbytes: int) -> int:
+        """Device pointer into the NVLS region (same offset on every rank when
+        all ranks allocate in the same order)."""
+        p = ctypes.c_void_p()
+        _check(library().lagom_comm_nvls_alloc(self._h, nbytes, ctypes.byref(p)), "nvls")
+        return p.value
+
+    def nvls_tensor(self, numel: int, dtype):
+        """A torch tensor whose storage is in the NVLS region (no copy)."""
+        import torch
+        typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<u2", torch.float16: "<f2",
+                   torch.int16: "<i2", torch.uint16: "<u2"}[dtype]
+        esize = torch.empty(0, dtype=dtype).element_size()
+        ptr = self.nvls_alloc(max(16, numel * esize))
+
+        class _View:
+            pass
+        v = _View()
+        v.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False), "version": 3}
+        t = torch.as_tensor(v, device="cuda")
+        if t.dtype != dtype:
+            t = t.view(dtype)
+        self._nvls_views = getattr(self, "_nvls_views", []) + [v]
+        return t
 
     @property
     def heap_bytes(self) -> int:

@@ -106,6 +106,7 @@ struct Comm {
   void* send = nullptr;
   void* recv = nullptr;
   std::int64_t in_elems = 0, out_elems = 0;
+  bool nvls = false;
 };
 
 template <typename T>
@@ -197,6 +198,7 @@ struct ReplayEngine::Impl {
   void* host_in = nullptr;   // pinned
   void* host_out = nullptr;  // pinned
   int calls = 0;
+  bool nvls_on = false;
 
   Impl(const ReplayDag& d, Coordinator& c, const ReplayOptions& o) : dag(d), coord(c), opts(o) {
     rank = coord.rank();
@@ -208,8 +210,8 @@ struct ReplayEngine::Impl {
     lt_check(cublasLtCreate(&lt), "cublasLtCreate");
     cuda_check(cudaMalloc(&workspace, workspace_bytes), "workspace");
     build_gemms();
-    build_comms();
     build_comm_backends();
+    build_comms();
     auto mk = [](cudaEvent_t* e) { cuda_check(cudaEventCreate(e), "event"); };
     mk(&ev_start);
     mk(&ev_cend);
@@ -258,6 +260,7 @@ struct ReplayEngine::Impl {
     for (auto& [k, p] : operands)
       for (void* q : p) cudaFree(q);
     for (Comm& c : comms) {
+      if (c.nvls) continue;  // owned by the communicator's NVLS region
       cudaFree(c.send);
       cudaFree(c.recv);
     }
@@ -360,8 +363,16 @@ struct ReplayEngine::Impl {
       c.in_elems = op.count * (in_full ? n : 1);
       c.out_elems = op.count * (out_full ? n : 1);
       const int e = elem_bytes(op.dtype);
-      cuda_check(cudaMalloc(&c.send, std::max<std::int64_t>(16, c.in_elems * e)), "comm send");
-      cuda_check(cudaMalloc(&c.recv, std::max<std::int64_t>(16, c.out_elems * e)), "comm recv");
+      const std::int64_t in_b = std::max<std::int64_t>(16, c.in_elems * e);
+      const std::int64_t out_b = std::max<std::int64_t>(16, c.out_elems * e);
+      if (nvls_on) {  // symmetric multicast region: TREE runs in the switch
+        coll_check(lagom_comm_nvls_alloc(lcomm, in_b, &c.send), "nvls alloc");
+        coll_check(lagom_comm_nvls_alloc(lcomm, out_b, &c.recv), "nvls alloc");
+        c.nvls = true;
+      } else {
+        cuda_check(cudaMalloc(&c.send, in_b), "comm send");
+        cuda_check(cudaMalloc(&c.recv, out_b), "comm recv");
+      }
       fill(c.send, c.in_elems, op.dtype, salt++);
       comms.push_back(c);
     }
@@ -380,6 +391,25 @@ struct ReplayEngine::Impl {
       std::vector<unsigned char> all(static_cast<std::size_t>(n) * LAGOM_HANDLE_BYTES);
       coord.allgather(mine, LAGOM_HANDLE_BYTES, all.data());
       coll_check(lagom_comm_import_handles(lcomm, all.data()), "import");
+    }
+    // NVLS region sized for every comm op's send + recv buffers (4 KiB aligned).
+    if (opts.nvls && n > 1 && lagom_comm_nvls_supported(lcomm)) {
+      std::int64_t need = 1 << 20;
+      for (const ReplayCommOp& op : dag.comm_ops) {
+        const bool in_full = op.collective == Collective::ReduceScatter || op.collective == Collective::AllToAll;
+        const bool out_full = op.collective == Collective::AllGather || op.collective == Collective::AllToAll;
+        const std::int64_t e = elem_bytes(op.dtype);
+        need += (op.count * e * (in_full ? n : 1) + 8191) / 4096 * 4096;
+        need += (op.count * e * (out_full ? n : 1) + 8191) / 4096 * 4096;
+      }
+      unsigned char blob[LAGOM_HANDLE_BYTES];
+      coll_check(lagom_comm_nvls_export(lcomm, need, blob), "nvls export");
+      coord.broadcast(blob, sizeof blob, 0);
+      coll_check(lagom_comm_nvls_import(lcomm, blob), "nvls import");
+      coord.barrier();
+      coll_check(lagom_comm_nvls_bind(lcomm), "nvls bind");
+      coord.barrier();
+      nvls_on = true;
     }
     if (opts.enable_nccl) {
       ncclUniqueId id{};

@@ -15,22 +15,7 @@
 
 using lagom_dev::KParams;
 
-struct lagom_comm {
-  int rank = 0;
-  int nranks = 1;
-  int device = 0;
-  bool virt = false;
-  bool ready = false;
-  lagom_comm_opts_t opts{};
-  int64_t slot_bytes = 0;
-  int64_t off_ready = 0, off_freed = 0, off_sstep = 0, off_rstep = 0, off_slots = 0;
-  int64_t heap_bytes = 0;
-  char* heap[LAGOM_MAX_RANKS] = {};  // mapped bases (own + peers / all virtual ranks)
-  bool imported[LAGOM_MAX_RANKS] = {};
-  unsigned int* abort_host = nullptr;
-  unsigned int* abort_dev = nullptr;
-  bool broken = false;
-};
+#include "comm_internal.h"
 
 namespace {
 
@@ -40,6 +25,9 @@ int fail(int status, const std::string& what) {
   g_last_error = what;
   return status;
 }
+}  // namespace
+int lagom_fail(int status, const std::string& what) { return fail(status, what); }
+namespace {
 
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(LAGOM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -63,6 +51,10 @@ void layout(lagom_comm* c) {
   off += ch * n * 8;
   c->off_rstep = off;
   off += ch * n * 8;
+  c->off_nvbar = off;  // NVLS entry/exit barrier flags [ch][src], 128 B apart
+  off += ch * n * 128;
+  c->off_nvep = off;   // NVLS per-channel epoch (local)
+  off += ch * 8;
   off = (off + 4095) / 4096 * 4096;
   c->off_slots = off;
   off += ch * n * c->opts.steps * c->slot_bytes;
@@ -102,6 +94,9 @@ int elem_bytes_of(int dtype) {
 // kernels_ll128.cu) so the 114 kernel instantiations compile in parallel.
 }  // namespace
 const void* lagom_pick_simple(int kind, int dtype, int op);
+int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
+                       const void** kernel, void* params_out, size_t* params_bytes);
+void lagom_nvls_release(lagom_comm* c);
 const void* lagom_pick_ll(int kind, int dtype, int op);
 const void* lagom_pick_ll128(int kind, int dtype, int op);
 namespace {
@@ -317,6 +312,7 @@ int lagom_comm_destroy(lagom_comm_t c) {
     if (c->virt || r == c->rank) cudaFree(c->heap[r]);
     else cudaIpcCloseMemHandle(c->heap[r]);
   }
+  lagom_nvls_release(c);
   if (c->abort_host) cudaFreeHost(c->abort_host);
   delete c;
   return LAGOM_OK;
@@ -355,6 +351,17 @@ int lagom_coll_launch(lagom_comm_t c, const lagom_coll_args_t* a, const void* se
     return fail(LAGOM_ERR_BROKEN, "communicator broken by an earlier abort");
   }
   if (a->count == 0) return LAGOM_OK;
+  {  // TREE on an NVSwitch box with NVLS bound: the switch-rooted schedule
+    alignas(16) unsigned char nv[512];
+    size_t nv_bytes = 0;
+    const void* nk = nullptr;
+    if (lagom_nvls_prepare(c, a, sendbuf, recvbuf, &nk, nv, &nv_bytes) == 1) {
+      void* nargs[] = {nv};
+      LAGOM_CUDA(cudaLaunchKernel(nk, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), nargs, 0,
+                                  static_cast<cudaStream_t>(stream)));
+      return LAGOM_OK;
+    }
+  }
   KParams p = make_params(c, a);
   p.send[0] = static_cast<const char*>(sendbuf);
   p.recv[0] = static_cast<char*>(recvbuf);

@@ -1,0 +1,37 @@
+// Internal: the communicator object shared by comm.cu and nvls.cu.
+#pragma once
+#include <cstdint>
+#include <string>
+
+#include "lagom_coll.h"
+
+struct lagom_comm {
+  int rank = 0;
+  int nranks = 1;
+  int device = 0;
+  bool virt = false;
+  bool ready = false;
+  lagom_comm_opts_t opts{};
+
+  int64_t slot_bytes = 0;
+  int64_t off_ready = 0, off_freed = 0, off_sstep = 0, off_rstep = 0, off_slots = 0;
+  int64_t heap_bytes = 0;
+  char* heap[LAGOM_MAX_RANKS] = {};  // mapped bases (own + peers / all virtual ranks)
+  bool imported[LAGOM_MAX_RANKS] = {};
+  unsigned int* abort_host = nullptr;
+  unsigned int* abort_dev = nullptr;
+  bool broken = false;
+  // NVLS (NVLink SHARP multicast): a symmetric region bound to a multicast
+  // object spanning every rank's GPU (nvls.cu).
+  unsigned long long nvls_mc_handle = 0;    // CUmemGenericAllocationHandle (multicast)
+  unsigned long long nvls_mem_handle = 0;   // CUmemGenericAllocationHandle (physical)
+  char* nvls_uc = nullptr;                  // unicast mapping of this rank's memory
+  char* nvls_mc = nullptr;                  // multicast mapping (all ranks)
+  int64_t nvls_bytes = 0;
+  int64_t nvls_used = 0;
+  bool nvls_ready = false;
+  int64_t off_nvbar = 0, off_nvep = 0;      // NVLS barrier flags / epochs in the heap
+};
+
+// Records `what` as lagom_last_error() and returns `status`.
+int lagom_fail(int status, const std::string& what);

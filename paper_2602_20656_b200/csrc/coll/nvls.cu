@@ -1,0 +1,411 @@
+// NVLS: collectives reduced / broadcast inside the NVSwitch (NVLink SHARP).
+//
+// On an NVSwitch box every rank reaches every other through the switch, so
+// the reference's TREE algorithm (Algorithm::Tree, model.hpp:37) is realized
+// with the switch as the tree's root: a multicast object spans one region of
+// every rank's HBM, `multimem.ld_reduce` returns the element-wise sum of all
+// ranks' copies (accumulated in fp32 for bf16/f16, in the switch), and
+// `multimem.st` writes one value into every rank's copy. Per GPU this moves
+// S bytes over NVLink for an AllReduce instead of the ring's 2(n-1)/n S
+// through the SMs, so far fewer channels (SMs) reach a given bandwidth —
+// which is exactly what the Lagom search trades against compute.
+//
+// Set-up is collective and transport-agnostic like the IPC heap: rank 0
+// creates the multicast object and exports a POSIX fd, peers duplicate it
+// with pidfd_getfd (blob = {pid, fd, size}), every rank adds its device, and
+// after a caller barrier every rank binds physical memory and maps both the
+// unicast and the multicast views. Buffers allocated from the region
+// (lagom_comm_nvls_alloc) have identical offsets on every rank.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstring>
+
+#include "comm_internal.h"
+#include "device.cuh"
+
+namespace {
+
+// Driver entry points are resolved at run time (cudaGetDriverEntryPoint), so
+// liblagom_coll.so loads on machines without a driver (CPU tests, build box).
+void* driver_sym(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return fn;
+}
+// decltype() names the prototype without referencing the symbol.
+#define DRV(fn) (reinterpret_cast<decltype(&fn)>(driver_sym(#fn)))
+
+
+constexpr uint64_t kBlobMagic = 0x4c41474f4d4e564cull;  // "LAGOMNVL"
+struct Blob {
+  uint64_t magic;
+  int64_t pid;
+  int64_t fd;
+  int64_t size;
+};
+
+int drv_fail(CUresult r, const char* what) {
+  const char* s = nullptr;
+  DRV(cuGetErrorString)(r, &s);
+  return lagom_fail(LAGOM_ERR_CUDA, std::string(what) + ": " + (s ? s : "?"));
+}
+#define LAGOM_DRV(call)                                  \
+  do {                                                   \
+    CUresult r_ = (call);                                \
+    if (r_ != CUDA_SUCCESS) return drv_fail(r_, #call);  \
+  } while (0)
+
+size_t granularity(int nranks) {
+  CUmulticastObjectProp prop{};
+  prop.numDevices = static_cast<unsigned>(nranks);
+  prop.size = 2u << 20;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g = 0;
+  if (DRV(cuMulticastGetGranularity)(&g, &prop, CU_MULTICAST_GRANULARITY_MINIMUM) != CUDA_SUCCESS || g == 0)
+    g = 2u << 20;
+  return g;
+}
+
+// --------------------------------------------------------------- kernels ---
+using lagom_dev::globaltimer;
+using lagom_dev::ld_acquire_sys;
+using lagom_dev::st_release_sys;
+
+struct NvlsParams {
+  char* heap[LAGOM_MAX_RANKS];
+  int rank, nranks;
+  int64_t count;        // elements, lagom_coll.h semantics
+  int elem_bytes;
+  const char* send_uc;  // local views
+  char* recv_uc;
+  char* send_mc;        // multicast views (send/recv inside the NVLS region)
+  char* recv_mc;
+  int64_t off_nvbar, off_nvep;
+  unsigned int* abort_flag;
+  uint64_t timeout_ns;
+  unsigned long long* span;
+};
+
+__device__ bool nv_wait(const uint64_t* p, uint64_t v, const NvlsParams& P) {
+  uint64_t t0 = 0;
+  unsigned it = 0;
+  while (ld_acquire_sys(p) < v) {
+    if ((++it & 127u) == 0) {
+      if (*reinterpret_cast<volatile unsigned*>(P.abort_flag)) return false;
+      const uint64_t now = globaltimer();
+      if (!t0) t0 = now;
+      if (now - t0 > P.timeout_ns) {
+        atomicExch(P.abort_flag, 1u);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+// All ranks' CTA `ch` meet: each posts `ep` into every peer's flag [ch][me]
+// and waits for every peer's post. Runs on thread 0.
+__device__ bool nv_barrier(const NvlsParams& P, int ch, uint64_t ep) {
+  const int n = P.nranks, r = P.rank;
+  for (int p = 0; p < n; ++p)
+    if (p != r)
+      st_release_sys(reinterpret_cast<uint64_t*>(P.heap[p] + P.off_nvbar + (static_cast<int64_t>(ch) * n + r) * 128), ep);
+  for (int p = 0; p < n; ++p)
+    if (p != r &&
+        !nv_wait(reinterpret_cast<const uint64_t*>(P.heap[r] + P.off_nvbar + (static_cast<int64_t>(ch) * n + p) * 128), ep, P))
+      return false;
+  return true;
+}
+
+template <typename T> struct Mm;
+template <> struct Mm<float> {
+  __device__ static uint4 ld_reduce(const void* p) {
+    uint4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+  }
+};
+template <> struct Mm<__nv_bfloat16> {
+  __device__ static uint4 ld_reduce(const void* p) {
+    uint4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+  }
+};
+template <> struct Mm<__half> {
+  __device__ static uint4 ld_reduce(const void* p) {
+    uint4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+  }
+};
+template <> struct Mm<int32_t> {
+  __device__ static uint4 ld_reduce(const void* p) {
+    const uint32_t* q = static_cast<const uint32_t*>(p);
+    uint4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.x) : "l"(q) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.y) : "l"(q + 1) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.z) : "l"(q + 2) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.w) : "l"(q + 3) : "memory");
+    return v;
+  }
+};
+__device__ __forceinline__ void mm_store(void* p, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+template <int KIND, typename T>
+__global__ void __launch_bounds__(640) nvls_kernel(const __grid_constant__ NvlsParams P) {
+  __shared__ int s_ok;
+  const int ch = blockIdx.x, nch = gridDim.x, n = P.nranks, r = P.rank;
+  if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
+  uint64_t* ep_home = reinterpret_cast<uint64_t*>(P.heap[r] + P.off_nvep + static_cast<int64_t>(ch) * 8);
+  const uint64_t ep = *reinterpret_cast<volatile uint64_t*>(ep_home) + 1;
+  if (threadIdx.x == 0) s_ok = nv_barrier(P, ch, ep) ? 1 : 0;  // every rank's inputs are ready
+  __syncthreads();
+  if (!s_ok) return;
+
+  // 16 B units: AR/RS reduce the whole buffer / own block through the switch,
+  // AG broadcasts the own block. Channel c owns a contiguous slice; in AR
+  // each rank further takes 1/n of it (its stores reach every rank).
+  const int64_t E = P.elem_bytes;
+  const int64_t B = P.count;  // elements per block (AR: the whole buffer)
+  const int64_t units = B * E / 16;
+  const int64_t per_ch = (units + nch - 1) / nch;
+  int64_t lo = lagom_dev::lmin(units, per_ch * ch), hi = lagom_dev::lmin(units, per_ch * (ch + 1));
+  if (KIND == 0) {  // AR: my 1/n share of the channel slice
+    const int64_t len = hi - lo, per_r = (len + n - 1) / n;
+    const int64_t a = lo + lagom_dev::lmin(len, per_r * r), b = lo + lagom_dev::lmin(len, per_r * (r + 1));
+    lo = a;
+    hi = b;
+  }
+  constexpr int U = 8;  // multimem loads are remote: keep 8 x 16 B in flight per thread
+  const int64_t blk = KIND == 0 ? 0 : static_cast<int64_t>(r) * units;  // block offset in units
+  for (int64_t u0 = lo + threadIdx.x; u0 < hi; u0 += static_cast<int64_t>(blockDim.x) * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t u = u0 + static_cast<int64_t>(k) * blockDim.x;
+      if (u < hi) {
+        if (KIND == 1) v[k] = reinterpret_cast<const uint4*>(P.send_uc)[u];
+        else v[k] = Mm<T>::ld_reduce(P.send_mc + (blk + u) * 16);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t u = u0 + static_cast<int64_t>(k) * blockDim.x;
+      if (u < hi) {
+        if (KIND == 0) mm_store(P.recv_mc + u * 16, v[k]);                // AR: to every rank
+        else if (KIND == 1) mm_store(P.recv_mc + (blk + u) * 16, v[k]);  // AG: block r everywhere
+        else reinterpret_cast<uint4*>(P.recv_uc)[u] = v[k];               // RS: my block, local
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // my multimem stores are visible everywhere
+    const bool ok = nv_barrier(P, ch, ep + 1);  // nobody reads results / reuses inputs early
+    if (ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+  }
+}
+
+template <int KIND>
+const void* pick_nvls(int dtype) {
+  switch (dtype) {
+    case LAGOM_F32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, float>);
+    case LAGOM_BF16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __nv_bfloat16>);
+    case LAGOM_F16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __half>);
+    case LAGOM_I32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, int32_t>);
+  }
+  return nullptr;
+}
+
+bool inside(const lagom_comm* c, const void* p, int64_t bytes) {
+  const char* q = static_cast<const char*>(p);
+  return c->nvls_ready && q >= c->nvls_uc && q + bytes <= c->nvls_uc + c->nvls_bytes;
+}
+
+int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 : 4; }
+
+}  // namespace
+
+// Used by lagom_coll_launch: 1 if this launch can run on the switch, with
+// *kernel/params filled in; 0 to fall back to the P2P kernels.
+int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
+                       const void** kernel, void* params_out, size_t* params_bytes) {
+  if (!c->nvls_ready || a->algorithm != LAGOM_TREE || a->redop != LAGOM_SUM || c->virt) return 0;
+  const int64_t e = ebytes(a->dtype), n = c->nranks;
+  int64_t in_b = 0, out_b = 0;
+  const void* k = nullptr;
+  switch (a->collective) {
+    case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype); break;
+    case LAGOM_ALL_GATHER: in_b = a->count * e; out_b = a->count * e * n; k = pick_nvls<1>(a->dtype); break;
+    case LAGOM_REDUCE_SCATTER: in_b = a->count * e * n; out_b = a->count * e; k = pick_nvls<2>(a->dtype); break;
+    default: return 0;
+  }
+  if ((a->count * e) % 16 != 0) return 0;  // whole 16 B units per block
+  const bool send_mc = a->collective != LAGOM_ALL_GATHER, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
+  if ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15) return 0;
+  if (send_mc && !inside(c, send, in_b)) return 0;
+  if (recv_mc && !inside(c, recv, out_b)) return 0;
+  NvlsParams p{};
+  for (int r = 0; r < c->nranks; ++r) p.heap[r] = c->heap[r];
+  p.rank = c->rank;
+  p.nranks = c->nranks;
+  p.count = a->count;
+  p.elem_bytes = static_cast<int>(e);
+  p.send_uc = static_cast<const char*>(send);
+  p.recv_uc = static_cast<char*>(recv);
+  p.send_mc = send_mc ? c->nvls_mc + (static_cast<const char*>(send) - c->nvls_uc) : nullptr;
+  p.recv_mc = recv_mc ? c->nvls_mc + (static_cast<char*>(recv) - c->nvls_uc) : nullptr;
+  p.off_nvbar = c->off_nvbar;
+  p.off_nvep = c->off_nvep;
+  p.abort_flag = c->abort_dev;
+  p.timeout_ns = static_cast<uint64_t>(c->opts.timeout_ms) * 1000000ull;
+  p.span = static_cast<unsigned long long*>(a->span_out);
+  std::memcpy(params_out, &p, sizeof p);
+  *params_bytes = sizeof p;
+  *kernel = k;
+  return 1;
+}
+
+extern "C" {
+
+int lagom_comm_nvls_supported(lagom_comm_t c) {
+  if (!c || c->virt || c->nranks < 2) return 0;
+  CUdevice dev;
+  int mc = 0;
+  if (DRV(cuDeviceGet)(&dev, c->device) != CUDA_SUCCESS) return 0;
+  if (DRV(cuDeviceGetAttribute)(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) != CUDA_SUCCESS) return 0;
+  return mc ? 1 : 0;
+}
+
+int lagom_comm_nvls_export(lagom_comm_t c, int64_t bytes, void* blob) {
+  if (!c || !blob || bytes <= 0) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_export: bad arguments");
+  std::memset(blob, 0, LAGOM_HANDLE_BYTES);
+  if (!lagom_comm_nvls_supported(c)) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "NVLS multicast unsupported");
+  if (c->rank != 0) return LAGOM_OK;
+  cudaSetDevice(c->device);
+  const size_t g = granularity(c->nranks);
+  CUmulticastObjectProp prop{};
+  prop.numDevices = static_cast<unsigned>(c->nranks);
+  prop.size = (static_cast<size_t>(bytes) + g - 1) / g * g;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUmemGenericAllocationHandle mc;
+  LAGOM_DRV(DRV(cuMulticastCreate)(&mc, &prop));
+  int fd = -1;
+  LAGOM_DRV(DRV(cuMemExportToShareableHandle)(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  c->nvls_mc_handle = mc;
+  c->nvls_bytes = static_cast<int64_t>(prop.size);
+  Blob b{kBlobMagic, static_cast<int64_t>(getpid()), fd, static_cast<int64_t>(prop.size)};
+  std::memcpy(blob, &b, sizeof b);
+  return LAGOM_OK;
+}
+
+int lagom_comm_nvls_import(lagom_comm_t c, const void* blob) {
+  if (!c || !blob) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_import: bad arguments");
+  Blob b;
+  std::memcpy(&b, blob, sizeof b);
+  if (b.magic != kBlobMagic) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_import: not an NVLS blob");
+  cudaSetDevice(c->device);
+  if (c->rank != 0) {
+    const int pidfd = static_cast<int>(syscall(SYS_pidfd_open, static_cast<pid_t>(b.pid), 0));
+    if (pidfd < 0) return lagom_fail(LAGOM_ERR_CUDA, "pidfd_open failed");
+    const int fd = static_cast<int>(syscall(SYS_pidfd_getfd, pidfd, static_cast<int>(b.fd), 0));
+    close(pidfd);
+    if (fd < 0) return lagom_fail(LAGOM_ERR_CUDA, "pidfd_getfd failed (ptrace permission?)");
+    CUmemGenericAllocationHandle mc;
+    const CUresult r = DRV(cuMemImportFromShareableHandle)(&mc, reinterpret_cast<void*>(static_cast<intptr_t>(fd)),
+                                                      CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(fd);
+    if (r != CUDA_SUCCESS) return drv_fail(r, "cuMemImportFromShareableHandle");
+    c->nvls_mc_handle = mc;
+    c->nvls_bytes = b.size;
+  }
+  CUdevice dev;
+  LAGOM_DRV(DRV(cuDeviceGet)(&dev, c->device));
+  LAGOM_DRV(DRV(cuMulticastAddDevice)(static_cast<CUmemGenericAllocationHandle>(c->nvls_mc_handle), dev));
+  return LAGOM_OK;
+}
+
+int lagom_comm_nvls_bind(lagom_comm_t c) {
+  if (!c || !c->nvls_mc_handle) return lagom_fail(LAGOM_ERR_NOT_READY, "nvls_bind before import");
+  cudaSetDevice(c->device);
+  const size_t size = static_cast<size_t>(c->nvls_bytes), g = granularity(c->nranks);
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUmemGenericAllocationHandle mem;
+  LAGOM_DRV(DRV(cuMemCreate)(&mem, size, &ap, 0));
+  c->nvls_mem_handle = mem;
+  const auto mc = static_cast<CUmemGenericAllocationHandle>(c->nvls_mc_handle);
+  LAGOM_DRV(DRV(cuMulticastBindMem)(mc, 0, mem, 0, size, 0));
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUdeviceptr uc = 0, mcv = 0;
+  LAGOM_DRV(DRV(cuMemAddressReserve)(&uc, size, g, 0, 0));
+  LAGOM_DRV(DRV(cuMemMap)(uc, size, 0, mem, 0));
+  LAGOM_DRV(DRV(cuMemSetAccess)(uc, size, &acc, 1));
+  LAGOM_DRV(DRV(cuMemAddressReserve)(&mcv, size, g, 0, 0));
+  LAGOM_DRV(DRV(cuMemMap)(mcv, size, 0, mc, 0));
+  LAGOM_DRV(DRV(cuMemSetAccess)(mcv, size, &acc, 1));
+  c->nvls_uc = reinterpret_cast<char*>(uc);
+  c->nvls_mc = reinterpret_cast<char*>(mcv);
+  if (cudaMemset(c->nvls_uc, 0, size) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return lagom_fail(LAGOM_ERR_CUDA, "nvls region init");
+  c->nvls_used = 0;
+  c->nvls_ready = true;
+  return LAGOM_OK;
+}
+
+int lagom_comm_nvls_alloc(lagom_comm_t c, int64_t bytes, void** ptr) {
+  if (!c || !ptr || bytes < 0) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_alloc: bad arguments");
+  if (!c->nvls_ready) return lagom_fail(LAGOM_ERR_NOT_READY, "NVLS region not bound");
+  const int64_t off = (c->nvls_used + 4095) / 4096 * 4096;
+  if (off + bytes > c->nvls_bytes) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "NVLS region exhausted");
+  c->nvls_used = off + bytes;
+  *ptr = c->nvls_uc + off;
+  return LAGOM_OK;
+}
+
+int64_t lagom_comm_nvls_bytes(lagom_comm_t c) { return c && c->nvls_ready ? c->nvls_bytes : 0; }
+
+}  // extern "C"
+
+void lagom_nvls_release(lagom_comm* c) {
+  if (!c) return;
+  if (c->nvls_mc) {
+    DRV(cuMemUnmap)(reinterpret_cast<CUdeviceptr>(c->nvls_mc), static_cast<size_t>(c->nvls_bytes));
+    DRV(cuMemAddressFree)(reinterpret_cast<CUdeviceptr>(c->nvls_mc), static_cast<size_t>(c->nvls_bytes));
+  }
+  if (c->nvls_uc) {
+    DRV(cuMemUnmap)(reinterpret_cast<CUdeviceptr>(c->nvls_uc), static_cast<size_t>(c->nvls_bytes));
+    DRV(cuMemAddressFree)(reinterpret_cast<CUdeviceptr>(c->nvls_uc), static_cast<size_t>(c->nvls_bytes));
+  }
+  if (c->nvls_mc_handle && c->nvls_mem_handle) {
+    CUdevice dev;
+    if (DRV(cuDeviceGet)(&dev, c->device) == CUDA_SUCCESS)
+      DRV(cuMulticastUnbind)(static_cast<CUmemGenericAllocationHandle>(c->nvls_mc_handle), dev, 0,
+                        static_cast<size_t>(c->nvls_bytes));
+  }
+  if (c->nvls_mem_handle) DRV(cuMemRelease)(static_cast<CUmemGenericAllocationHandle>(c->nvls_mem_handle));
+  if (c->nvls_mc_handle) DRV(cuMemRelease)(static_cast<CUmemGenericAllocationHandle>(c->nvls_mc_handle));
+  c->nvls_mc = c->nvls_uc = nullptr;
+  c->nvls_ready = false;
+}

@@ -145,7 +145,7 @@ class PyEngine {
  public:
   PyEngine(const std::string& dag_json, const std::string& coord_name, int rank, int size, int device,
            int repeats, int warmup, bool nccl, std::int64_t max_chunk, int max_channels,
-           std::int64_t e2e_in, std::int64_t e2e_out, bool reserve)
+           std::int64_t e2e_in, std::int64_t e2e_out, bool reserve, bool nvls)
       : dag_(dag_from_json(parse(dag_json))) {
     coord_ = b200::make_shm_coordinator(coord_name, rank, size);
     b200::ReplayOptions o;
@@ -158,6 +158,7 @@ class PyEngine {
     o.e2e_in_bytes = e2e_in;
     o.e2e_out_bytes = e2e_out;
     o.reserve_comm_sms = reserve;
+    o.nvls = nvls;
     engine_ = std::make_unique<b200::ReplayEngine>(dag_, *coord_, o);
   }
   std::string workload(const std::string& gpu_json) const {
@@ -324,11 +325,11 @@ PYBIND11_MODULE(_lagom_py, m) {
 
   py::class_<PyEngine>(m, "ReplayEngine")
       .def(py::init<const std::string&, const std::string&, int, int, int, int, int, bool, std::int64_t, int,
-                    std::int64_t, std::int64_t, bool>(),
+                    std::int64_t, std::int64_t, bool, bool>(),
            py::arg("dag"), py::arg("coord_name"), py::arg("rank"), py::arg("size"), py::arg("device"),
            py::arg("repeats") = 3, py::arg("warmup") = 1, py::arg("nccl") = true,
            py::arg("max_chunk_bytes") = 4 << 20, py::arg("max_channels") = 32, py::arg("e2e_in_bytes") = 0,
-           py::arg("e2e_out_bytes") = 0, py::arg("reserve_comm_sms") = false)
+           py::arg("e2e_out_bytes") = 0, py::arg("reserve_comm_sms") = false, py::arg("nvls") = false)
       .def("workload", &PyEngine::workload, py::arg("gpu") = "")
       .def("run", &PyEngine::run)
       .def("run_e2e", &PyEngine::run_e2e)

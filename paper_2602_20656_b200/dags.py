@@ -129,6 +129,15 @@ def mixtral_ep(nranks: int, layers: int = 32):
     return {"name": f"mixtral-8x7b-ep{n}", "parallelism": f"ep{n}", "compute_ops": compute, "comm_ops": comm}
 
 
+def with_nc_max(dag: dict, nc_max: int) -> dict:
+    """Per-op resource bounds (reference CommBounds, model.hpp:70-76): the
+    reference default nc_max = 32 was sized for its modeled 64-SM device; on
+    a 148-SM B200 the search may use up to 64 channels."""
+    for c in dag["comm_ops"]:
+        c.setdefault("bounds", {})["nc_max"] = nc_max
+    return dag
+
+
 BUILDERS = {"gpt2-1.3b-dp": gpt2_dp, "llama3-8b-tp-sp": llama8b_tp_sp,
             "llama3-70b-fsdp": llama70b_fsdp, "mixtral-8x7b-ep": mixtral_ep}
 

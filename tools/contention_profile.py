@@ -83,6 +83,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="profiles/fitted_params.json")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--nvls", type=int, default=1, help="TREE = in-switch (NVLS) when the box supports it")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -102,14 +103,14 @@ def main():
     gemm = [8192, 8192, 2048]  # a 275 GFLOP compute-bound victim op (x8 per replay)
     dag = dag_for(sizes, gemm)
     eng = L.ReplayEngine(json.dumps(dag), f"lagom_cp_{token}", rank, world, local, repeats=3, warmup=1,
-                         nccl=False, reserve_comm_sms=True)
+                         nccl=False, reserve_comm_sms=True, nvls=bool(a.nvls), max_channels=64)
     if rank != 0:
         eng.serve()
         eng.close()
         if world > 1:
             dist.barrier()
         return
-    ncs = [1, 2, 4, 8, 16, 32]
+    ncs = [1, 2, 4, 8, 16, 32, 64]
     nts = [64, 256, 640]
     chunks = [32 * KIB, 256 * KIB, 1 * MIB, 4 * MIB]
     keys = [("RING", "SIMPLE"), ("RING", "LL"), ("RING", "LL128"), ("TREE", "SIMPLE")]
@@ -136,16 +137,14 @@ def main():
     eng.stop()
     eng.close()
 
-    # ---- fits
-    link_guess = max(m / x for pts in meas.values() for (_, _, _, m, x) in pts)  # bytes/us
+    # ---- fits (median-relative-error least squares, tools/predict_vs_measured.fit)
+    from tools.predict_vs_measured import fit as fit_model
     params, report = {}, {}
     for key, pts in meas.items():
-        co, link, err = fit_comm(pts, link_guess)
-        rel = [abs(predict(co, link, *p[:4]) - p[4]) / p[4] for p in pts]
+        co, link, rep = fit_model(pts)
         co.update({"mem_coeff": 0.5, "chunk_knee": 128 * KIB})
         params[key] = co
-        report[key] = {"link_bw": link, "rms_rel_err": err, "median_rel_err": float(np.median(rel)),
-                       "p90_rel_err": float(np.percentile(rel, 90)), "points": len(pts)}
+        report[key] = dict(rep, link_bw=link)
     # victim: SM loss lambda/(lambda-NC) explains part of the slowdown; the
     # remainder is attributed to the comm's HBM footprint V (wave_time's
     # blocks*D/(B - V) term) -> kappa, C_knee for RING/SIMPLE.
@@ -171,7 +170,7 @@ def main():
     params["RING/SIMPLE/P2P"]["mem_coeff"] = kappa
     params["RING/SIMPLE/P2P"]["chunk_knee"] = int(knee)
     params["collective_factors"] = {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0}
-    gpu = {"num_sms": lam, "peak_mem_bw": peak, "link_bw": report["RING/SIMPLE/P2P"]["link_bw"],
+    gpu = {"num_sms": lam, "peak_mem_bw": peak, "link_bw": max(r["link_bw"] for r in report.values()),
            "comm_bw_cap_fraction": 0.6, "compute_on_comm_slowdown": 0.0}
     # validate the params document with the product loader (reference schema)
     L.tune_sim(json.dumps({"gpu": gpu, "compute_ops": [{"id": "c", "total_blocks": 1, "blocks_per_sm": 1,
