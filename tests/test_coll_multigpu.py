@@ -25,13 +25,18 @@ def _gpus():
         return 0
 
 
+@pytest.mark.parametrize("nvls", [0, 1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_real_multigpu_parity(world):
+def test_real_multigpu_parity(world, nvls):
+    """nvls=1: buffers in a multicast region, so TREE AllReduce runs inside
+    the NVSwitch (int32 and movement bit-exact; fp sums within the stated
+    tolerance, since the switch accumulates in fp32 in its own order)."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, LAGOM_NVLS="1") if nvls else dict(os.environ)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
