@@ -335,6 +335,12 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "note": f"n=1 collective = local copy; peak = {peaks['_source']} copy bandwidth"}
+    # The Lagom picks run the collective on a few SMs by design; the per-SM
+    # rate against the per-SM share of the peak shows how hard those SMs work.
+    nc_dom = int(tuned["configs"][groups[j_dom]]["num_channels"])
+    roof["channels"] = nc_dom
+    roof["achieved_per_sm"] = roof["achieved"] / max(1, nc_dom)
+    roof["peak_per_sm_share"] = roof["peak"] / n_sms if world == 1 else roof["peak"] / max(1, nc_dom)
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
