@@ -31,7 +31,7 @@ CU_SRCS    := $(wildcard $(PKG)/csrc/coll/*.cu)
 CU_OBJS    := $(patsubst $(PKG)/csrc/coll/%.cu,build/coll/%.o,$(CU_SRCS))
 
 .PHONY: all host coll b200 py oracle clean
-all: host coll b200 py build/parity_driver build/table_tune
+all: host coll b200 py cli build/parity_driver build/table_tune
 
 host: $(PKG)/liblagom.so
 
@@ -73,6 +73,13 @@ build/b200/%.o: $(PKG)/csrc/b200/%.cpp $(wildcard $(PKG)/csrc/b200/*.hpp) $(wild
 
 $(PKG)/liblagom_b200.so: $(B200_OBJS) $(PKG)/liblagom.so $(PKG)/liblagom_coll.so
 	$(CXX) -shared -o $@ $(B200_OBJS) -L$(PKG) -llagom -llagom_coll $(CUDA_LIBS) -Wl,-rpath,'$$ORIGIN'
+
+# The reference CLI's surface (simulate|tune|oracle|compare|sweep|gen) + tune --profiler gpu
+cli: build/lagom
+
+build/lagom: $(PKG)/csrc/cli/lagom_cli.cpp $(PKG)/liblagom.so $(PKG)/liblagom_b200.so $(wildcard include/lagom/*.hpp)
+	@mkdir -p build
+	$(CXX) $(HOST_FLAGS) $(CUDA_INC) $< -L$(PKG) -llagom_b200 -llagom -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 py: $(PKG)/_lagom_py$(PYEXT)
 

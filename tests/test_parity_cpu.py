@@ -81,14 +81,14 @@ def test_product_bytes_equal_reference_build(product_lines):
 
 
 SUITES = ["test_model", "test_commperf", "test_contention", "test_simulator", "test_tuner",
-          "test_oracle", "test_workloads"]
+          "test_oracle", "test_workloads", "test_cli"]
 
 
 @pytest.fixture(scope="module")
 def conformance_build():
     if not os.path.isdir(REF_TESTS):
         pytest.skip("/root/reference not present")
-    subprocess.run(["make", "-C", ROOT, "host"], check=True, capture_output=True)
+    subprocess.run(["make", "-C", ROOT, "host", "cli"], check=True, capture_output=True)
     r = subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp"), "-j8"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-3000:]
     return os.path.join(ROOT, "build", "conformance")
@@ -96,7 +96,8 @@ def conformance_build():
 
 @pytest.mark.parametrize("suite", SUITES)
 def test_reference_unit_suite_passes_against_product(conformance_build, suite):
-    env = dict(os.environ, LAGOM_DATA=os.path.join(ROOT, "data"))
+    # test_cli drives our `lagom` binary (reference tests/CMakeLists.txt:20-25 sets LAGOM_BIN)
+    env = dict(os.environ, LAGOM_DATA=os.path.join(ROOT, "data"), LAGOM_BIN=os.path.join(ROOT, "build", "lagom"))
     r = subprocess.run([os.path.join(conformance_build, suite)], capture_output=True, text=True, env=env,
                        timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
