@@ -340,7 +340,8 @@ def main():
     nc_dom = int(tuned["configs"][groups[j_dom]]["num_channels"])
     roof["channels"] = nc_dom
     roof["achieved_per_sm"] = roof["achieved"] / max(1, nc_dom)
-    roof["peak_per_sm_share"] = roof["peak"] / n_sms if world == 1 else roof["peak"] / max(1, nc_dom)
+    if world == 1:  # HBM is shared by all SMs: compare with one SM's share
+        roof["peak_per_sm_share"] = roof["peak"] / n_sms
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
@@ -389,6 +390,14 @@ def main():
     }
     print(json.dumps(line), flush=True)
     if args.out:
+        # measured Chrome traces (reference trace schema) of one Lagom and one NCCL step
+        for arm in ("lagom", "nccl"):
+            if result[arm]:
+                with open(args.out.replace(".json", f"_trace_{arm}.json"), "w") as f:
+                    json.dump(result[arm][len(result[arm]) // 2].get("trace", []), f)
+        for arm in ("lagom", "e2e", "seed", "nccl", "compute", "comm"):
+            for r in result[arm]:
+                r.pop("trace", None)
         with open(args.out, "w") as f:
             json.dump({"line": line, "tune": tuned, "tune_runs": tune_runs, "raw": result}, f)
 

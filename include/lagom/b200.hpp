@@ -117,6 +117,10 @@ struct ReplayMeasurement {
   ProfileResult profile;           // x_j, X = sum x_j, Y = sum y_i, Z
   std::vector<double> comp_times;  // y_i
   double wall_us = 0.0;            // host wall time of the profile call
+  // This rank's last replay as a timeline (one event per compute op on the
+  // "compute" stream, one per comm op on "comm"), start offsets from the
+  // replay start — exportable with trace_to_json (reference json_io.hpp:36).
+  std::vector<TimelineEvent> timeline;
 };
 
 class ReplayEngine {

@@ -199,6 +199,7 @@ struct ReplayEngine::Impl {
   void* host_out = nullptr;  // pinned
   int calls = 0;
   bool nvls_on = false;
+  std::vector<TimelineEvent> last_timeline;
 
   Impl(const ReplayDag& d, Coordinator& c, const ReplayOptions& o) : dag(d), coord(c), opts(o) {
     rank = coord.rank();
@@ -574,6 +575,14 @@ struct ReplayEngine::Impl {
       for (std::size_t i = 0; i < M; ++i) out[N + i] = us(ev_cb[i], ev_ce[i]);
     z = std::max(us(ev_start, ev_cend), us(ev_start, ev_kend));
     out[N + M] = z;
+    last_timeline.clear();
+    if (do_compute)
+      for (std::size_t i = 0; i < M; ++i)
+        last_timeline.push_back({"compute", dag.compute_ops[i].id, us(ev_start, ev_cb[i]), out[N + i],
+                                 static_cast<std::int64_t>(gemms[i].size())});
+    if (do_comm)
+      for (std::size_t j = 0; j < N; ++j)
+        last_timeline.push_back({"comm", dag.comm_ops[j].id, us(ev_start, ev_kb[j]), out[j], 0});
     return out;
   }
 
@@ -612,6 +621,7 @@ struct ReplayEngine::Impl {
     m.profile.total_compute = 0.0;
     for (double y : m.comp_times) m.profile.total_compute += y;
     m.profile.makespan = med(N + M);
+    m.timeline = last_timeline;
     ++calls;
     m.wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     if (trace_on())

@@ -135,8 +135,11 @@ GpuSpec gpu_from_json(const std::string& s) {
 }
 
 Json measurement_json(const b200::ReplayMeasurement& m) {
+  SimResult tl;
+  tl.timeline = m.timeline;
   return Json{{"x", m.profile.comm_times}, {"y", m.comp_times}, {"X", m.profile.total_comm},
-              {"Y", m.profile.total_compute}, {"Z", m.profile.makespan}, {"wall_us", m.wall_us}};
+              {"Y", m.profile.total_compute}, {"Z", m.profile.makespan}, {"wall_us", m.wall_us},
+              {"trace", trace_to_json(tl)}};
 }
 
 std::vector<CommConfig> configs_arg(const std::string& s) { return configs_from_json(parse(s)); }
