@@ -46,3 +46,23 @@ def test_tune_and_replay_modes(engine):
     r = json.loads(L.tune_table(json.dumps(t["workload"]), json.dumps(t["initial"]),
                                 json.dumps(t["profile_table"]), 12))
     assert r["configs"] == t["configs"]
+
+
+def test_cli_tune_with_gpu_profiler(engine, tmp_path):
+    """`lagom tune --profiler gpu` (the reference CLI surface with the replay
+    engine as profiler) on one GPU."""
+    import subprocess
+    from tests.conftest import ROOT
+    eng, dag = engine
+    w = tmp_path / "w.json"
+    d = tmp_path / "d.json"
+    w.write_text(eng.workload(""))
+    d.write_text(json.dumps(dag))
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", LAGOM_JOB=f"clitest{os.getpid()}")
+    r = subprocess.run([os.path.join(ROOT, "build", "lagom"), "tune", "--workload", str(w), "--dag", str(d),
+                        "--profiler", "gpu", "--budget", "4", "--start", "nccl-default"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode in (0, 4), r.stderr[-2000:]
+    rep = json.loads(r.stdout)
+    assert rep["command"] == "tune" and 1 <= rep["profile_calls"] <= 4
+    assert len(rep["configs"]) == len(dag["comm_ops"])
