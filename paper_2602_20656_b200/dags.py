@@ -7,10 +7,10 @@ attached: cuBLASLt bf16 GEMMs [m, n, k(, batch)] per compute op, and one
 collective per comm op (bf16, counts per include/lagom_coll.h). Shapes follow
 the public model cards; data is synthetic (random-init on device).
 
-``window`` builds the two-layer tuning window used to search configs: the
-layers of every config are identical, so a comm op's config found on the
-window is applied to the same comm role (bucket / position) in every layer of
-the full DAG, which the timed steps replay in full.
+Every comm op carries a ``role`` (its position in the layer: the k-th
+gradient bucket, the attention/MLP AG or RS, dispatch/combine): bench.py
+tunes one config per role against the full iteration (the reference tuner
+over grouped comm ops, lagom::b200::make_grouped_gpu_profiler).
 """
 from __future__ import annotations
 
@@ -140,35 +140,6 @@ def with_nc_max(dag: dict, nc_max: int) -> dict:
 
 BUILDERS = {"gpt2-1.3b-dp": gpt2_dp, "llama3-8b-tp-sp": llama8b_tp_sp,
             "llama3-70b-fsdp": llama70b_fsdp, "mixtral-8x7b-ep": mixtral_ep}
-
-
-def window(dag: dict, layers: int = 2) -> dict:
-    """The tuning window: the first `layers` compute ops' layers and the comm
-    ops gated on them (plus ungated leading comms)."""
-    keep_compute = dag["compute_ops"][: layers * _compute_per_layer(dag)]
-    ids = {c["id"] for c in keep_compute}
-    last = keep_compute[-1]["id"]
-    comm = []
-    for c in dag["comm_ops"]:
-        if c.get("ready_after") is None or c["ready_after"] in ids:
-            if c.get("ready_after") == last:
-                continue  # would not overlap anything inside the window
-            comm.append(c)
-    return {"name": dag["name"] + "-window", "compute_ops": keep_compute, "comm_ops": comm}
-
-
-def _compute_per_layer(dag):
-    return 2 if dag["name"].startswith("llama3-8b") else 1
-
-
-def expand_configs(dag: dict, win: dict, win_configs: list) -> list:
-    """Map configs tuned on the window to every comm op of the full DAG by
-    comm role (bucket index / position in the layer)."""
-    by_role = {}
-    for c, cfg in zip(win["comm_ops"], win_configs):
-        by_role.setdefault(c.get("role", 0), cfg)
-    fallback = win_configs[0]
-    return [by_role.get(c.get("role", 0), fallback) for c in dag["comm_ops"]]
 
 
 def flops(dag: dict) -> float:

@@ -1,6 +1,2 @@
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
-timeout 900 $CMD > gpurun_out/plain_n1.log 2>&1 && timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n1.csv $CMD > gpurun_out/ncu_launches_n1.log 2>&1; echo "ncu launches exit $?"
-K="python tools/coll_kernel_run.py --coll AR --algo 1 --ranks 1 --count 13107200 --nc 8 --nt 512 --chunk 2M"
-$K > gpurun_out/k_tree1.log 2>&1 && cat gpurun_out/k_tree1.log && ncu --set full --clock-control none --import-source on -k regex:coll_kernel -s 5 -c 1 -o gpurun_out/prof_tree_n1 $K > gpurun_out/ncu_tree1.log 2>&1; echo "ncu full exit $?"
-K4="python tools/coll_kernel_run.py --coll AR --algo 0 --ranks 4 --count 13107200 --nc 8 --nt 512 --chunk 2M"
-$K4 > gpurun_out/k_ring4.log 2>&1 && cat gpurun_out/k_ring4.log && ncu --set full --clock-control none --import-source on -k regex:coll_kernel -s 5 -c 1 -o gpurun_out/prof_ring_v4 $K4 > gpurun_out/ncu_ring4.log 2>&1; echo "ncu full4 exit $?"
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"; tail -1 gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
