@@ -61,7 +61,7 @@ $(PKG)/liblagom_coll.so: $(CU_OBJS)
 
 # B200 layer: replay engine, shm coordinator, NCCL (dlopen) baseline.
 B200_SRCS  := $(wildcard $(PKG)/csrc/b200/*.cpp)
-B200_OBJS  := $(patsubst $(PKG)/csrc/b200/%.cpp,build/b200/%.o,$(B200_SRCS))
+B200_OBJS  := $(patsubst $(PKG)/csrc/b200/%.cpp,build/b200/%.o,$(B200_SRCS)) build/b200/exhaustive_gpu.o
 CUDA_INC   := -I$(CUDA_HOME)/include
 CUDA_LIBS  := -L$(CUDA_HOME)/lib64 -lcudart -lcublasLt -ldl -lrt
 
@@ -70,6 +70,11 @@ b200: $(PKG)/liblagom_b200.so
 build/b200/%.o: $(PKG)/csrc/b200/%.cpp $(wildcard $(PKG)/csrc/b200/*.hpp) $(wildcard include/lagom/*.hpp) include/lagom_coll.h
 	@mkdir -p build/b200
 	$(CXX) $(HOST_FLAGS) $(CUDA_INC) -c $< -o $@
+
+# --fmad=false: the GPU exhaustive oracle must round like the host simulator
+build/b200/exhaustive_gpu.o: $(PKG)/csrc/b200/exhaustive_gpu.cu $(wildcard include/lagom/*.hpp)
+	@mkdir -p build/b200
+	$(NVCC) -std=c++20 -O3 $(CU_ARCH) --fmad=false -Xcompiler -fPIC -Iinclude -I$(NLOHMANN) -c $< -o $@
 
 $(PKG)/liblagom_b200.so: $(B200_OBJS) $(PKG)/liblagom.so $(PKG)/liblagom_coll.so
 	$(CXX) -shared -o $@ $(B200_OBJS) -L$(PKG) -llagom -llagom_coll $(CUDA_LIBS) -Wl,-rpath,'$$ORIGIN'

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "lagom/model.hpp"
+#include "lagom/oracle.hpp"
 #include "lagom/simulator.hpp"
 #include "lagom/tuner.hpp"
 
@@ -183,6 +184,13 @@ Workload grouped_workload(const ReplayDag& dag, const std::vector<int>& group_of
                           int nranks);
 ProfileFn make_grouped_gpu_profiler(ReplayEngine& engine, std::vector<int> group_of_op,
                                     std::vector<std::pair<std::vector<CommConfig>, ProfileResult>>* record = nullptr);
+
+// exhaustive() (reference oracle.cpp:12-63) with one GPU thread per joint
+// grid point; bit-identical result (FP64, no FMA contraction, host argmin in
+// enumeration order). Falls back to the CPU oracle for what it does not cover
+// (more than 64 ops, invalid grid entries, grids beyond `limit`).
+lagom::OracleResult exhaustive_gpu(const Workload& workload, const std::vector<std::vector<CommConfig>>& grids,
+                            const SubspaceParams& params, std::int64_t limit, int device = 0);
 
 // A ProfileFn that answers from a recorded table (exact config-vector match;
 // throws Error(InvalidInput) on a miss). Used to prove that two tuners make

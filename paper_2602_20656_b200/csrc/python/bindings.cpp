@@ -296,6 +296,14 @@ PYBIND11_MODULE(_lagom_py, m) {
     const TuneResult r = tune(wl, configs_arg(init), b200::make_table_profiler(std::move(t)), budget);
     return tune_json(wl, r, 0.0).dump();
   }, py::arg("workload"), py::arg("initial"), py::arg("table"), py::arg("budget") = 500);
+  m.def("oracle_gpu", [](const std::string& w, const std::string& p, std::int64_t limit, int device) {
+    const Workload wl = workload_from_json(parse(w));
+    const SubspaceParams params = params_or_default(p);
+    py::gil_scoped_release nogil;
+    const OracleResult o = b200::exhaustive_gpu(wl, default_grids(wl, params), params, limit, device);
+    return Json{{"Z", o.makespan}, {"evaluations", o.evaluations},
+                {"configs", configs_to_json(o.configs)["configs"]}}.dump();
+  }, py::arg("workload"), py::arg("params") = "", py::arg("limit") = 1000000, py::arg("device") = 0);
   m.def("oracle", [](const std::string& w, const std::string& p, std::int64_t limit) {
     const Workload wl = workload_from_json(parse(w));
     const SubspaceParams params = params_or_default(p);

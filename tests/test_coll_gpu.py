@@ -105,3 +105,41 @@ def test_virtual_parity_data_paths(case, use_tma):
             assert got[r].tobytes() == want[r].tobytes(), f"rank {r} differs"
     finally:
         vc.close()
+
+
+@pytest.mark.parametrize("offset_elems", [1, 3, 8])
+@pytest.mark.parametrize("proto", [0, 1, 2])
+@pytest.mark.parametrize("coll,algo", [(0, 0), (0, 1), (1, 0), (2, 0), (3, 0)])
+def test_misaligned_user_buffers(vcomms, coll, algo, proto, offset_elems):
+    """User buffers that start off a 16-byte boundary (torch views at an
+    element offset) take the byte-granular load/store paths and bypass TMA;
+    results must still be bit-exact."""
+    import torch
+    from paper_2602_20656_b200 import coll as C
+    from tests.oracle_ref import in_elems
+    n, dtype, count = 3, C.BF16, 5000 + 7
+    rng = np.random.default_rng(coll * 100 + proto * 10 + offset_elems)
+    from tests.oracle_ref import random_input
+    sends = [random_input(dtype, in_elems(coll, n, count), rng) for _ in range(n)]
+    want = oracle_collective(coll, algo, dtype, 0, sends)
+    dev, outs = [], []
+    for s in sends:
+        base = torch.zeros(s.size + offset_elems, dtype=torch.uint16, device="cuda")
+        base[offset_elems:] = torch.from_numpy(s).cuda()
+        dev.append(base[offset_elems:])
+        ob = torch.full((out_elems(coll, n, count) + offset_elems,), 0xABAB, dtype=torch.uint16, device="cuda")
+        outs.append(ob[offset_elems:])
+    cfg = C.CollConfig(algo, proto, 4, 256, 8192)
+    vcomms[n].launch(coll, cfg, dtype, count, [t.data_ptr() for t in dev], [t.data_ptr() for t in outs],
+                     torch.cuda.current_stream().cuda_stream, 0)
+    torch.cuda.synchronize()
+    vcomms[n].check()
+    for r in range(n):
+        assert outs[r].cpu().numpy().tobytes() == want[r].tobytes()
+
+
+def test_zero_count_is_a_no_op(vcomms):
+    from paper_2602_20656_b200 import coll as C
+    for coll in range(4):
+        vcomms[2].launch(coll, C.CollConfig(C.RING, C.SIMPLE, 2, 64, 32768), C.F32, 0, [0, 0], [0, 0])
+    vcomms[2].check()

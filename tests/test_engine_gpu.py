@@ -66,3 +66,23 @@ def test_cli_tune_with_gpu_profiler(engine, tmp_path):
     rep = json.loads(r.stdout)
     assert rep["command"] == "tune" and 1 <= rep["profile_calls"] <= 4
     assert len(rep["configs"]) == len(dag["comm_ops"])
+
+
+def test_gpu_batched_exhaustive_matches_cpu_oracle():
+    """exhaustive() with one GPU thread per joint grid point
+    returns the CPU oracle's bits (makespan, evaluations, argmin configs)."""
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_20656_b200 import _lagom_py as L
+    cases = [L.gen("allreduce-pair"), L.gen("fsdp", layers=1, seed=5), L.gen("tp", layers=2, seed=3)]
+    cases += [L.gen("random", seed=s, m=1 + s % 4, n=1 + s % 3) for s in range(20)]
+    for s in (3, 7):  # delta > 0 exercises the stretch integration
+        w = json.loads(L.gen("random", seed=100 + s, m=3, n=2))
+        w["gpu"]["compute_on_comm_slowdown"] = 0.2 * s
+        cases.append(json.dumps(w))
+    for w in cases:
+        cpu = json.loads(L.oracle(w, "", 10 ** 7))
+        gpu = json.loads(L.oracle_gpu(w, "", 10 ** 7, 0))
+        assert gpu["evaluations"] == cpu["evaluations"]
+        assert gpu["Z"] == cpu["Z"]  # bit-identical doubles
+        assert gpu["configs"] == cpu["configs"]
