@@ -1,10 +1,12 @@
-timeout 900 python -m pytest tests/test_coll_gpu.py tests/test_engine_gpu.py -m gpu -q --timeout 600 -p no:cacheprovider -k "misaligned or zero_count or exhaustive or tune_and_replay or cli" > gpurun_out/pytest_new.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_new.log
-python - <<'PY'
-import json, time
-from paper_2602_20656_b200 import _lagom_py as L
-w = L.gen("fsdp", layers=2, seed=7)
-t0 = time.perf_counter(); c = json.loads(L.oracle(w, "", 10**8)); t1 = time.perf_counter()
-g = json.loads(L.oracle_gpu(w, "", 10**8, 0)); t2 = time.perf_counter()
-g = json.loads(L.oracle_gpu(w, "", 10**8, 0)); t3 = time.perf_counter()
-print("points", c["evaluations"], "cpu_s", round(t1-t0,3), "gpu_s(first)", round(t2-t1,3), "gpu_s", round(t3-t2,3), "identical", c == g)
+N=4
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29711 tools/contention_profile.py --out gpurun_out/cprof_final_n4.json > gpurun_out/cprof_final_n4.log 2>&1; echo "cprof exit $?"
+for N in 4 2; do
+for W in gpt2-1.3b-dp llama3-8b-tp-sp llama3-70b-fsdp mixtral-8x7b-ep; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 2972$N bench.py --gpus $N --steps 8 --warmup 3 --workload $W --params gpurun_out/cprof_final_n4.json --out gpurun_out/final_n${N}_$W.json > gpurun_out/final_n${N}_$W.log 2>&1; echo "$N $W exit $?"
+python - <<PY
+import json
+d=json.load(open("gpurun_out/final_n${N}_$W.json"))["line"]
+t=d["config"]["tune"]
+print("N=$N $W", "lagom", round(d["value"],2), "nccl", round(d["nccl_default_ms"],2), "x", round(d["speedup_vs_nccl_default"],3), "start", t["start"], t["picks"][:2], "slow", round(d["compute"]["slowdown"],3), round(d["compute"]["slowdown_nccl"],3), "roof", round(d["roofline"]["frac"],3))
 PY
+done; done
