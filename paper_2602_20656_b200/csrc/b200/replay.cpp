@@ -403,14 +403,24 @@ struct ReplayEngine::Impl {
         need += (op.count * e * (in_full ? n : 1) + 8191) / 4096 * 4096;
         need += (op.count * e * (out_full ? n : 1) + 8191) / 4096 * 4096;
       }
+      // Every step is agreed on by all ranks (max-reduce of a failure flag):
+      // if any rank cannot create, import or bind the multicast region, all
+      // ranks fall back to the P2P kernels together instead of hanging.
+      auto agree = [&](bool ok) {
+        double bad = ok ? 0.0 : 1.0;
+        coord.allreduce_max(&bad, 1);
+        return bad == 0.0;
+      };
       unsigned char blob[LAGOM_HANDLE_BYTES];
-      coll_check(lagom_comm_nvls_export(lcomm, need, blob), "nvls export");
-      coord.broadcast(blob, sizeof blob, 0);
-      coll_check(lagom_comm_nvls_import(lcomm, blob), "nvls import");
-      coord.barrier();
-      coll_check(lagom_comm_nvls_bind(lcomm), "nvls bind");
-      coord.barrier();
-      nvls_on = true;
+      bool ok = agree(lagom_comm_nvls_export(lcomm, need, blob) == LAGOM_OK);
+      if (ok) {
+        coord.broadcast(blob, sizeof blob, 0);
+        ok = agree(lagom_comm_nvls_import(lcomm, blob) == LAGOM_OK);
+      }
+      if (ok) ok = agree(lagom_comm_nvls_bind(lcomm) == LAGOM_OK);
+      nvls_on = ok;
+      if (!ok && rank == 0 && trace_on())
+        std::fprintf(stderr, "[lagom] NVLS unavailable (%s); TREE uses the P2P kernels\n", lagom_last_error());
     }
     if (opts.enable_nccl) {
       ncclUniqueId id{};

@@ -31,6 +31,7 @@ struct lagom_comm {
   int64_t nvls_used = 0;
   bool nvls_ready = false;
   int64_t off_nvbar = 0, off_nvep = 0;      // NVLS barrier flags / epochs in the heap
+  int nvls_export_fd = -1;                  // rank 0's exported fd, closed once bound
 };
 
 // Records `what` as lagom_last_error() and returns `status`.

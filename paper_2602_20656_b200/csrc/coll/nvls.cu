@@ -309,6 +309,7 @@ int lagom_comm_nvls_export(lagom_comm_t c, int64_t bytes, void* blob) {
   LAGOM_DRV(DRV(cuMemExportToShareableHandle)(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
   c->nvls_mc_handle = mc;
   c->nvls_bytes = static_cast<int64_t>(prop.size);
+  c->nvls_export_fd = fd;
   Blob b{kBlobMagic, static_cast<int64_t>(getpid()), fd, static_cast<int64_t>(prop.size)};
   std::memcpy(blob, &b, sizeof b);
   return LAGOM_OK;
@@ -371,6 +372,12 @@ int lagom_comm_nvls_bind(lagom_comm_t c) {
     return lagom_fail(LAGOM_ERR_CUDA, "nvls region init");
   c->nvls_used = 0;
   c->nvls_ready = true;
+  // Binding is collective (every rank imported before anyone binds), so the
+  // exported fd has served its purpose.
+  if (c->nvls_export_fd >= 0) {
+    close(c->nvls_export_fd);
+    c->nvls_export_fd = -1;
+  }
   return LAGOM_OK;
 }
 
@@ -390,6 +397,10 @@ int64_t lagom_comm_nvls_bytes(lagom_comm_t c) { return c && c->nvls_ready ? c->n
 
 void lagom_nvls_release(lagom_comm* c) {
   if (!c) return;
+  if (c->nvls_export_fd >= 0) {
+    close(c->nvls_export_fd);
+    c->nvls_export_fd = -1;
+  }
   if (c->nvls_mc) {
     DRV(cuMemUnmap)(reinterpret_cast<CUdeviceptr>(c->nvls_mc), static_cast<size_t>(c->nvls_bytes));
     DRV(cuMemAddressFree)(reinterpret_cast<CUdeviceptr>(c->nvls_mc), static_cast<size_t>(c->nvls_bytes));
