@@ -185,7 +185,8 @@ def main():
                     help="subspace params fitted on B200 by tools/contention_profile.py (reference JSON "
                          "schema); '' = the reference's synthetic defaults")
     ap.add_argument("--sm-reserve", type=int, default=1,
-                    help="Lagom replays run GEMMs on num_sms - max NC SMs (cuBLASLt SM count target)")
+                    help="Lagom replays run each compute op's GEMMs on num_sms - max NC of the collectives "
+                         "that can overlap it (cuBLASLt SM count target)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -366,7 +367,8 @@ def main():
         "config": {"workload": dag["name"], "compute_ops": len(dag["compute_ops"]),
                    "comm_ops": len(dag["comm_ops"]), "parallelism": dag.get("parallelism", f"dp{world}"),
                    "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
-                   "sm_partition": "GEMMs on num_sms - max NC" if args.sm_reserve else "none",
+                   "sm_partition": "per compute op: GEMMs on num_sms - max NC of overlappable collectives"
+                   if args.sm_reserve else "none",
                    "params": os.path.relpath(args.params, ROOT) if args.params else "reference defaults",
                    "nvls": bool(args.nvls) and world > 1,
                    "tune": {"start": tuned["start"], "others": tuned["other_starts"],

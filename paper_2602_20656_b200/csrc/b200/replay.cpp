@@ -512,16 +512,23 @@ struct ReplayEngine::Impl {
   // One replay on this rank; returns [x_0..x_{N-1}, y_0..y_{M-1}, Z] in us.
   std::vector<double> replay(Mode mode, const std::vector<CommConfig>* cfgs) {
     const bool do_compute = mode != Mode::CommOnly;
-    // SM partition (opts.reserve_comm_sms): Lagom modes run the GEMMs on
-    // num_sms - max NC so the collective's CTAs never queue behind them.
-    int sm_target = 0;
-    if (opts.reserve_comm_sms && cfgs && (mode == Mode::Lagom || mode == Mode::LagomE2E)) {
-      int nc = 0;
-      for (const CommConfig& c : *cfgs) nc = std::max(nc, c.num_channels);
-      sm_target = std::max(1, num_sms - nc);
-    }
     const bool do_comm = mode != Mode::ComputeOnly;
     const std::size_t M = dag.compute_ops.size(), N = comms.size();
+    // SM partition (opts.reserve_comm_sms): in Lagom modes compute op i runs
+    // its GEMMs on num_sms - (max NC of the collectives that can overlap it),
+    // so those CTAs never queue behind the GEMMs. Collective j, gated on
+    // compute op d (or ungated, d = -1), can only run during ops i > d; ops
+    // no collective can overlap (e.g. before the first gate) keep the whole
+    // GPU, and collectives gated on the last op cost the GEMMs nothing.
+    std::vector<int> sm_target(M, 0);
+    if (opts.reserve_comm_sms && cfgs && (mode == Mode::Lagom || mode == Mode::LagomE2E)) {
+      std::vector<int> reserve(M, 0);
+      for (std::size_t j = 0; j < N; ++j)
+        for (std::size_t i = static_cast<std::size_t>(comms[j].dep + 1); i < M; ++i)
+          reserve[i] = std::max(reserve[i], (*cfgs)[j].num_channels);
+      for (std::size_t i = 0; i < M; ++i)
+        if (reserve[i] > 0) sm_target[i] = std::max(1, num_sms - reserve[i]);
+    }
     coord.barrier();
     const bool e2e = mode == Mode::LagomE2E;
     cuda_check(cudaEventRecord(ev_start, cs), "record");
@@ -539,7 +546,7 @@ struct ReplayEngine::Impl {
     if (do_compute) {
       for (std::size_t i = 0; i < M; ++i) {
         cuda_check(cudaEventRecord(ev_cb[i], cs), "record");
-        for (Gemm& g : gemms[i]) launch_gemm(g, sm_target);
+        for (Gemm& g : gemms[i]) launch_gemm(g, sm_target[i]);
         cuda_check(cudaEventRecord(ev_ce[i], cs), "record");
       }
     }

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -161,6 +162,13 @@ int smem_for(const KParams& p, const lagom_coll_args_t* a, const void* kernel) {
   return groups * kTmaStages * 3 * p.tile_bytes;
 }
 
+// TMA share of a split copy step in LSU-thread equivalents (device.cuh,
+// KParams::tma_share_*); environment overrides for experiments.
+int tma_share(const char* env, int dflt) {
+  const char* e = std::getenv(env);
+  return e ? std::max(0, std::atoi(e)) : dflt;
+}
+
 KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
   KParams p{};
   for (int r = 0; r < c->nranks; ++r) p.heap[r] = c->heap[r];
@@ -182,6 +190,8 @@ KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
   p.tma = (c->opts.use_tma && a->protocol == LAGOM_SIMPLE) ? 1 : 0;
   p.tma_stages = kTmaStages;
   p.tma_reduce = c->opts.use_tma >= 2 ? 1 : 0;
+  p.tma_share_local = tma_share("LAGOM_TMA_SHARE_LOCAL", 0);
+  p.tma_share_push = tma_share("LAGOM_TMA_SHARE_PUSH", 0);
   // 192 KB of tile ring per CTA: 3 buffers x stages per group (2 groups for tree)
   const int groups = (a->collective == LAGOM_ALL_REDUCE && a->algorithm == LAGOM_TREE) ? 2 : 1;
   p.tile_bytes = kTmaSmemBytes / (groups * kTmaStages * 3) / 1024 * 1024;

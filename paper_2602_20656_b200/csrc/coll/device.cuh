@@ -57,6 +57,12 @@ struct KParams {
   int tma_stages;            // smem ring depth per group
   int tile_bytes;            // bytes per TMA tile (per input buffer)
   int tma_reduce;            // also route reduction steps through the TMA ring
+  // Copy steps split their bytes between the TMA engine (warp 0) and the LSU
+  // threads of the other warps, in proportion to measured rates: the TMA
+  // engine of one SM moves as much as `tma_share_*` LSU threads (local copy /
+  // push to a peer). 0: the TMA ring takes the whole 16 B aligned body.
+  int tma_share_local;
+  int tma_share_push;
 };
 
 // ------------------------------------------------------------------ TMA ----
@@ -323,13 +329,22 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
   bool ok = true;
 
   int64_t lsu_from = 0;  // units already moved by the TMA path
+  int ltid = g.tid, ln = g.n;  // the LSU part's threads (all, or warps 1..)
   if constexpr (PROTO == LAGOM_SIMPLE) {
     constexpr int NIN = NR + (SRC ? 1 : 0);
     // TMA moves copy steps (one input); reduction steps use it only when
     // P.tma_reduce is set (measured slower than the LSU path on B200 so far).
     if (P.tma && g.smem && NIN > 0 && (NIN == 1 || P.tma_reduce) && (!SRC || src_al) && (!DST || dst_al) &&
         nbytes >= 16) {
-      const int64_t main = nbytes & ~static_cast<int64_t>(15);
+      int64_t main = nbytes & ~static_cast<int64_t>(15);
+      if (NIN == 1) {
+        const int share = NS > 0 ? P.tma_share_push : P.tma_share_local;
+        if (share > 0 && g.n >= 64) {  // warp 0 drives TMA, warps 1.. run the LSU loop
+          main = (main * share / (share + g.n - 32)) & ~static_cast<int64_t>(15);
+          ltid = g.tid - 32;
+          ln = g.n - 32;
+        }
+      }
       const int T = P.tile_bytes, ST = P.tma_stages;
       const int64_t ntiles = (main + T - 1) / T;
       const uint32_t base = *reinterpret_cast<volatile uint32_t*>(g.tiles);
@@ -437,28 +452,30 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
       lsu_from = main >> 4;
     }
   }
-  if constexpr (PROTO == LAGOM_SIMPLE) {
+  if (PROTO == LAGOM_SIMPLE && ltid < 0) {
+    // TMA driver warp of a split copy: its bytes are done (thread 0 waited).
+  } else if constexpr (PROTO == LAGOM_SIMPLE) {
     // Fast path (all user pointers 16 B aligned): batches of U whole units per
     // thread, every load of the batch issued before any combine or store so
     // each thread keeps U (or 2U) 16 B requests in flight.
     constexpr int U = (NR + (SRC ? 1 : 0) >= 2) ? 4 : 8;
     const int64_t whole = nbytes >> 4;
-    int64_t u0 = lsu_from + g.tid;
+    int64_t u0 = lsu_from + ltid;
     if ((!SRC || src_al) && (!DST || dst_al)) {
-      const int64_t stride = static_cast<int64_t>(g.n) * U;
-      for (; u0 + static_cast<int64_t>(U - 1) * g.n < whole; u0 += stride) {
+      const int64_t stride = static_cast<int64_t>(ln) * U;
+      for (; u0 + static_cast<int64_t>(U - 1) * ln < whole; u0 += stride) {
         uint4 own[U];
         uint4 in[NR > 0 ? NR : 1][U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
-          const int64_t u = u0 + static_cast<int64_t>(k) * g.n;
+          const int64_t u = u0 + static_cast<int64_t>(k) * ln;
           if (SRC) own[k] = reinterpret_cast<const uint4*>(src)[u];
 #pragma unroll
           for (int i = 0; i < NR; ++i) in[i][k] = ld_stage(reinterpret_cast<const uint4*>(rs[i]) + u);
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
-          const int64_t u = u0 + static_cast<int64_t>(k) * g.n;
+          const int64_t u = u0 + static_cast<int64_t>(k) * ln;
           uint4 v = SRC ? own[k] : in[0][k];
 #pragma unroll
           for (int i = SRC ? 0 : 1; i < NR; ++i) v = red4<R>(v, in[i][k]);
@@ -469,7 +486,7 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
       }
     }
     // Remainder, partial last unit, misaligned user buffers.
-    for (int64_t u = u0; u < units; u += g.n) {
+    for (int64_t u = u0; u < units; u += ln) {
       const int nb = static_cast<int>(lmin(16, nbytes - u * 16));
       uint4 v = make_uint4(0, 0, 0, 0);
       if (SRC) v = load_user(src + u * 16, nb, src_al);
@@ -643,25 +660,67 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
   return true;
 }
 
-// Plain local copy by a group (own block of AllToAll / single-rank cases):
-// 8 x 16 B loads in flight per thread when both sides are 16 B aligned.
-__device__ __forceinline__ void group_copy(const Grp& g, const char* src, char* dst, int64_t nbytes) {
+// Plain local copy by a group (own block of AllToAll / single-rank cases).
+// With the TMA ring (SIMPLE, P.tma) one elected thread streams part of the
+// 16 B aligned body through the smem stages (bulk load -> bulk store) while
+// warps 1.. copy the rest with 8 x 16 B loads in flight per thread; the split
+// follows P.tma_share_local, so small CTAs (the Lagom search starts at
+// NT = 64) still move ~50 GB/s and large ones add the LSU rate on top.
+__device__ __forceinline__ void group_copy(const Grp& g, const KParams& P, const char* src, char* dst,
+                                           int64_t nbytes) {
   constexpr int U = 8;
   const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  int64_t done = 0;  // bytes moved by the TMA ring
+  int ltid = g.tid, ln = g.n;
+  if (P.tma && g.smem && al && nbytes >= 16) {
+    done = nbytes & ~static_cast<int64_t>(15);
+    if (P.tma_share_local > 0 && g.n >= 64) {
+      done = (done * P.tma_share_local / (P.tma_share_local + g.n - 32)) & ~static_cast<int64_t>(15);
+      ltid = g.tid - 32;
+      ln = g.n - 32;
+    }
+    if (g.tid == 0 && done > 0) {
+      const int T = P.tile_bytes, ST = P.tma_stages;
+      const int64_t ntiles = (done + T - 1) / T;
+      const uint32_t base = *reinterpret_cast<volatile uint32_t*>(g.tiles);
+      auto buf = [&](uint32_t stage) { return g.smem + static_cast<int64_t>(stage) * 3 * T; };
+      auto issue = [&](int64_t i) {
+        const uint32_t stg = (base + static_cast<uint32_t>(i)) % ST;
+        const uint32_t len = static_cast<uint32_t>(lmin(T, done - i * T));
+        mbar_expect(&g.bars[stg], len);
+        bulk_load(buf(stg), src + i * T, len, &g.bars[stg]);
+      };
+      for (int64_t i = 0; i < ntiles && i < ST; ++i) issue(i);
+      for (int64_t i = 0; i < ntiles; ++i) {
+        const uint32_t gi = base + static_cast<uint32_t>(i);
+        const uint32_t stg = gi % ST;
+        mbar_wait(&g.bars[stg], (gi / ST) & 1u);
+        bulk_store(dst + i * T, buf(stg), static_cast<uint32_t>(lmin(T, done - i * T)));
+        bulk_commit();
+        if (i >= 1 && i - 1 + ST < ntiles) {
+          bulk_wait_read1();  // tile i-1's store has read its stage
+          issue(i - 1 + ST);
+        }
+      }
+      bulk_wait_all();
+      *reinterpret_cast<volatile uint32_t*>(g.tiles) = base + static_cast<uint32_t>(ntiles);
+    }
+  }
   const int64_t units = (nbytes + 15) >> 4, whole = nbytes >> 4;
-  int64_t u0 = g.tid;
+  if (ltid < 0) return;  // TMA driver warp
+  int64_t u0 = (done >> 4) + ltid;
   if (al) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (; u0 + static_cast<int64_t>(U - 1) * g.n < whole; u0 += static_cast<int64_t>(g.n) * U) {
+    for (; u0 + static_cast<int64_t>(U - 1) * ln < whole; u0 += static_cast<int64_t>(ln) * U) {
       uint4 v[U];
 #pragma unroll
-      for (int k = 0; k < U; ++k) v[k] = s4[u0 + static_cast<int64_t>(k) * g.n];
+      for (int k = 0; k < U; ++k) v[k] = s4[u0 + static_cast<int64_t>(k) * ln];
 #pragma unroll
-      for (int k = 0; k < U; ++k) d4[u0 + static_cast<int64_t>(k) * g.n] = v[k];
+      for (int k = 0; k < U; ++k) d4[u0 + static_cast<int64_t>(k) * ln] = v[k];
     }
   }
-  for (int64_t u = u0; u < units; u += g.n) {
+  for (int64_t u = u0; u < units; u += ln) {
     const int nb = static_cast<int>(lmin(16, nbytes - u * 16));
     store_user(dst + u * 16, load_user(src + u * 16, nb, al), nb, al);
   }
@@ -706,7 +765,7 @@ __device__ void ring_allgather(const Grp& g, const KParams& P, int r, int ch, in
   char* recv = P.recv[P.rank < 0 ? r : 0];
   const Slice sl = channel_slice(B, E, nch, ch);
   if (n == 1) {
-    group_copy(g, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
+    group_copy(g, P, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
     return;
   }
   RecvLink in = make_recv(P, r, ch, (r + n - 1) % n);
@@ -735,7 +794,7 @@ __device__ void ring_reducescatter(const Grp& g, const KParams& P, int r, int ch
   char* recv = P.recv[P.rank < 0 ? r : 0];
   const Slice sl = channel_slice(B, E, nch, ch);
   if (n == 1) {
-    group_copy(g, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
+    group_copy(g, P, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
     return;
   }
   RecvLink in = make_recv(P, r, ch, (r + n - 1) % n);
@@ -764,7 +823,7 @@ __device__ void ring_allreduce(const Grp& g, const KParams& P, int r, int ch, in
   char* recv = P.recv[P.rank < 0 ? r : 0];
   if (n == 1) {
     const Slice sl = channel_slice(N, E, nch, ch);
-    group_copy(g, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
+    group_copy(g, P, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
     return;
   }
   const int64_t B = ring_block(N, n, E);
@@ -826,7 +885,12 @@ __device__ void tree_allreduce(const KParams& P, int r, int ch, int nch, volatil
   const Slice sl = channel_slice(N, E, nch, ch);
   if (n == 1) {
     Grp all{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 1, aborts};
-    group_copy(all, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
+    if (smem) {
+      all.smem = smem;
+      all.bars = bars[0];
+      all.tiles = tiles;
+    }
+    group_copy(all, P, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
     return;
   }
   const int half = blockDim.x / 2;
@@ -896,7 +960,7 @@ __device__ void alltoall(const Grp& g, const KParams& P, int r, int ch, int nch)
   }
   for (int64_t off = sl.lo; off < sl.hi; off += ce) {
     const int64_t nb = lmin(ce, sl.hi - off) * E;
-    group_copy(g, send + (r * B + off) * E, recv + (r * B + off) * E, nb);
+    group_copy(g, P, send + (r * B + off) * E, recv + (r * B + off) * E, nb);
     for (int p = 1; p < n; ++p) {
       const int d = (r + p) % n, s = (r - p + n) % n;
       if (!step<PROTO, NoRed, 0, true, false, 1>(g, P, nullptr, &out[p], send + (d * B + off) * E, nullptr, nb)) return;

@@ -22,6 +22,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "comm_internal.h"
@@ -165,8 +166,8 @@ __device__ __forceinline__ void mm_store(void* p, uint4 v) {
                : "memory");
 }
 
-template <int KIND, typename T>
-__global__ void __launch_bounds__(640) nvls_kernel(const __grid_constant__ NvlsParams P) {
+template <int KIND, typename T, int U, int MAXT>
+__global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ NvlsParams P) {
   __shared__ int s_ok;
   const int ch = blockIdx.x, nch = gridDim.x, n = P.nranks, r = P.rank;
   if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
@@ -190,28 +191,32 @@ __global__ void __launch_bounds__(640) nvls_kernel(const __grid_constant__ NvlsP
     lo = a;
     hi = b;
   }
-  constexpr int U = 8;  // multimem loads are remote: keep 8 x 16 B in flight per thread
+  // multimem loads are remote: U x 16 B in flight per thread
   const int64_t blk = KIND == 0 ? 0 : static_cast<int64_t>(r) * units;  // block offset in units
-  for (int64_t u0 = lo + threadIdx.x; u0 < hi; u0 += static_cast<int64_t>(blockDim.x) * U) {
+  // Pointers are advanced per batch so the unrolled body needs no 64-bit
+  // index math or bounds checks (keeps U = 16 free of spills at 640 threads).
+  const int64_t nt = blockDim.x;
+  const char* in = KIND == 1 ? P.send_uc : P.send_mc + blk * 16;
+  char* out = KIND == 2 ? P.recv_uc : P.recv_mc + blk * 16;
+  auto load = [&](const char* p) -> uint4 {
+    if (KIND == 1) return *reinterpret_cast<const uint4*>(p);
+    return Mm<T>::ld_reduce(p);
+  };
+  auto store = [&](char* p, uint4 v) {
+    if (KIND == 2) *reinterpret_cast<uint4*>(p) = v;  // RS: my block, local
+    else mm_store(p, v);                              // AR / AG: to every rank
+  };
+  int64_t u0 = lo + threadIdx.x;
+  for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+    const char* src = in + u0 * 16;
+    char* dst = out + u0 * 16;
     uint4 v[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t u = u0 + static_cast<int64_t>(k) * blockDim.x;
-      if (u < hi) {
-        if (KIND == 1) v[k] = reinterpret_cast<const uint4*>(P.send_uc)[u];
-        else v[k] = Mm<T>::ld_reduce(P.send_mc + (blk + u) * 16);
-      }
-    }
+    for (int k = 0; k < U; ++k) v[k] = load(src + k * nt * 16);
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t u = u0 + static_cast<int64_t>(k) * blockDim.x;
-      if (u < hi) {
-        if (KIND == 0) mm_store(P.recv_mc + u * 16, v[k]);                // AR: to every rank
-        else if (KIND == 1) mm_store(P.recv_mc + (blk + u) * 16, v[k]);  // AG: block r everywhere
-        else reinterpret_cast<uint4*>(P.recv_uc)[u] = v[k];               // RS: my block, local
-      }
-    }
+    for (int k = 0; k < U; ++k) store(dst + k * nt * 16, v[k]);
   }
+  for (; u0 < hi; u0 += nt) store(out + u0 * 16, load(in + u0 * 16));
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();  // my multimem stores are visible everywhere
@@ -221,15 +226,38 @@ __global__ void __launch_bounds__(640) nvls_kernel(const __grid_constant__ NvlsP
   }
 }
 
-template <int KIND>
-const void* pick_nvls(int dtype) {
+template <int KIND, int U, int MAXT>
+const void* pick_nvls_u(int dtype) {
   switch (dtype) {
-    case LAGOM_F32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, float>);
-    case LAGOM_BF16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __nv_bfloat16>);
-    case LAGOM_F16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __half>);
-    case LAGOM_I32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, int32_t>);
+    case LAGOM_F32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, float, U, MAXT>);
+    case LAGOM_BF16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __nv_bfloat16, U, MAXT>);
+    case LAGOM_F16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __half, U, MAXT>);
+    case LAGOM_I32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, int32_t, U, MAXT>);
   }
   return nullptr;
+}
+// Requests in flight per thread. multimem.ld_reduce is a round trip through
+// the switch, so AR / RS throughput per SM is set by the bytes in flight,
+// NT x U x 16 B (measured on 4xB200: AR 25 MiB at NC = 4, NT = 512 goes from
+// 232 to 411 GB/s busbw with U = 16 instead of 8). Small CTAs (the Lagom
+// search starts at NT = 64) get a deeper unroll so they are not starved:
+// NT <= 256 -> U = 32 (128 data registers, launch bound 256); else U = 16.
+// Large-NT AG only needs U = 8 (its loads are local). LAGOM_NVLS_UNROLL = 4 | 8 | 16 forces one
+// unroll at every NT (experiments).
+template <int KIND>
+const void* pick_nvls(int dtype, int nt) {
+  static const int forced = [] {
+    const char* e = std::getenv("LAGOM_NVLS_UNROLL");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 4 || v == 8 || v == 16) ? v : 0;
+  }();
+  switch (forced) {
+    case 4: return pick_nvls_u<KIND, 4, 640>(dtype);
+    case 8: return pick_nvls_u<KIND, 8, 640>(dtype);
+    case 16: return pick_nvls_u<KIND, 16, 640>(dtype);
+  }
+  if (nt <= 256) return pick_nvls_u<KIND, 32, 256>(dtype);
+  return KIND == 1 ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
 }
 
 bool inside(const lagom_comm* c, const void* p, int64_t bytes) {
@@ -250,9 +278,9 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   int64_t in_b = 0, out_b = 0;
   const void* k = nullptr;
   switch (a->collective) {
-    case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype); break;
-    case LAGOM_ALL_GATHER: in_b = a->count * e; out_b = a->count * e * n; k = pick_nvls<1>(a->dtype); break;
-    case LAGOM_REDUCE_SCATTER: in_b = a->count * e * n; out_b = a->count * e; k = pick_nvls<2>(a->dtype); break;
+    case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype, a->num_threads); break;
+    case LAGOM_ALL_GATHER: in_b = a->count * e; out_b = a->count * e * n; k = pick_nvls<1>(a->dtype, a->num_threads); break;
+    case LAGOM_REDUCE_SCATTER: in_b = a->count * e * n; out_b = a->count * e; k = pick_nvls<2>(a->dtype, a->num_threads); break;
     default: return 0;
   }
   if ((a->count * e) % 16 != 0) return 0;  // whole 16 B units per block

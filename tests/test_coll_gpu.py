@@ -29,20 +29,31 @@ def vcomms():
         c.close()
 
 
+GUARD = 4096  # bytes of canary on both sides of every output buffer
+
+
 def run_virtual(vc, c, sends_np):
+    """One virtual launch. Besides the result it checks what compute-sanitizer
+    would (closed on this pool): no byte outside an output buffer is written
+    (canary bands on both sides) and no input byte changes."""
     import torch
     from paper_2602_20656_b200 import coll as C
     n = c["n"]
     dev = [torch.from_numpy(s).cuda() for s in sends_np]
-    outs = [torch.full((out_elems(c["coll"], n, c["count"]),), 0, dtype=dev[0].dtype, device="cuda")
-            for _ in range(n)]
-    for o in outs:
-        o.view(torch.uint8).fill_(0xAB)  # poison: every byte must be written
+    nbytes = out_elems(c["coll"], n, c["count"]) * sends_np[0].itemsize
+    bases = [torch.full((GUARD + nbytes + GUARD,), 0x5A, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    for b in bases:
+        b[GUARD:GUARD + nbytes].fill_(0xAB)  # poison: every byte must be written
+    outs = [b[GUARD:GUARD + nbytes].view(dev[0].dtype) for b in bases]
     cfg = C.CollConfig(c["algo"], c["proto"], c["nc"], c["nt"], c["chunk"])
     vc.launch(c["coll"], cfg, c["dtype"], c["count"], [t.data_ptr() for t in dev],
               [t.data_ptr() for t in outs], torch.cuda.current_stream().cuda_stream, c["op"])
     torch.cuda.synchronize()
     vc.check()
+    for r, b in enumerate(bases):
+        assert bool((b[:GUARD] == 0x5A).all()) and bool((b[GUARD + nbytes:] == 0x5A).all()), \
+            f"rank {r}: write outside the output buffer"
+        assert dev[r].cpu().numpy().tobytes() == sends_np[r].tobytes(), f"rank {r}: input modified"
     return [o.cpu().numpy() for o in outs]
 
 
@@ -122,13 +133,17 @@ def test_misaligned_user_buffers(vcomms, coll, algo, proto, offset_elems):
     from tests.oracle_ref import random_input
     sends = [random_input(dtype, in_elems(coll, n, count), rng) for _ in range(n)]
     want = oracle_collective(coll, algo, dtype, 0, sends)
-    dev, outs = [], []
+    dev, outs, guards = [], [], []
     for s in sends:
         base = torch.zeros(s.size + offset_elems, dtype=torch.uint16, device="cuda")
         base[offset_elems:] = torch.from_numpy(s).cuda()
         dev.append(base[offset_elems:])
-        ob = torch.full((out_elems(coll, n, count) + offset_elems,), 0xABAB, dtype=torch.uint16, device="cuda")
-        outs.append(ob[offset_elems:])
+        m = out_elems(coll, n, count)
+        ob = torch.full((m + offset_elems + 64,), 0xABAB, dtype=torch.uint16, device="cuda")
+        ob[:offset_elems] = 0x5A5A
+        ob[offset_elems + m:] = 0x5A5A  # canaries on both sides
+        guards.append(ob)
+        outs.append(ob[offset_elems:offset_elems + m])
     cfg = C.CollConfig(algo, proto, 4, 256, 8192)
     vcomms[n].launch(coll, cfg, dtype, count, [t.data_ptr() for t in dev], [t.data_ptr() for t in outs],
                      torch.cuda.current_stream().cuda_stream, 0)
@@ -136,6 +151,8 @@ def test_misaligned_user_buffers(vcomms, coll, algo, proto, offset_elems):
     vcomms[n].check()
     for r in range(n):
         assert outs[r].cpu().numpy().tobytes() == want[r].tobytes()
+        g = guards[r].cpu().numpy()
+        assert (g[:offset_elems] == 0x5A5A).all() and (g[offset_elems + outs[r].numel():] == 0x5A5A).all()
 
 
 def test_zero_count_is_a_no_op(vcomms):

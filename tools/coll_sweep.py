@@ -56,12 +56,13 @@ def main():
     ap.add_argument("--nccl", type=int, default=1)
     ap.add_argument("--out", default="")
     ap.add_argument("--nvls", type=int, default=0, help="buffers in an NVLS region (TREE runs in-switch)")
+    ap.add_argument("--use-tma", type=int, default=1, help="SIMPLE data path: 0 LSU, 1 TMA copies, 2 TMA also reduces")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = C.Communicator.from_process_group(device=local, max_channels=64)
+    comm = C.Communicator.from_process_group(device=local, max_channels=64, use_tma=args.use_tma)
     stream = torch.cuda.current_stream()
     s_ptr = stream.cuda_stream
     if args.nvls:
@@ -113,6 +114,7 @@ def main():
                 else:
                     ok = bool(((y.float() - y_ref).abs() <= (2.0 ** -7) * world * mag + 1e-6).all())
                 rows.append(dict(impl="lagom", ok=ok, coll=cn, algo=int(algo), proto=int(proto), nc=int(nc), nt=int(nt),
+                                 use_tma=args.use_tma,
                                  chunk=parse_size(ch), bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
                                  busbw=s_bytes / t * fac / 1e9))
                 if rank == 0:
