@@ -250,6 +250,7 @@ def main():
             pj = json.loads(params_doc)
             params_doc = json.dumps(pj.get("params", pj))  # accept a profile file or a bare table
         runs = {st: json.loads(eng.tune(gpu_json, st, args.budget, params_doc, groups)) for st in starts}
+        tune_wall_s = time.perf_counter() - t_tune
         eng.set_measurement(1, 0)
         # The replays are noisy under the 1 kW power cap, so the starts' final
         # assignments are compared head to head (interleaved) before choosing.
@@ -285,10 +286,14 @@ def main():
             for fn in arms.values():
                 fn()
         runs = {k: [] for k in arms}
+        # The arm order rotates every step: on a power-capped part a replay
+        # runs faster right after a lighter one, so no arm keeps a fixed
+        # predecessor.
+        names = list(arms)
         with ClockSampler(local) as clk:
-            for _ in range(args.steps):
-                for k, fn in arms.items():
-                    runs[k].append(json.loads(fn()))
+            for s in range(args.steps):
+                for k in names[s % len(names):] + names[:s % len(names)]:
+                    runs[k].append(json.loads(arms[k]()))
         lagom_runs, e2e_runs, seed_runs = runs["lagom"], runs["e2e"], runs["seed"]
         nccl_runs = runs.get("nccl", [])
         compute_only = series(eng.run_compute_only, max(3, args.steps // 3))
@@ -375,6 +380,9 @@ def main():
                             "groups": len(tuned["configs"]),
                             "profile_calls": tuned["profile_calls"], "boundary": tuned["boundary_condition"],
                             "search_wall_s": round(tune_wall_s, 3),
+                            "search_calls_total": sum(r["profile_calls"] for r in tune_runs.values()),
+                            "ms_per_profile_call": round(1e3 * tune_wall_s /
+                                                         max(1, sum(r["profile_calls"] for r in tune_runs.values())), 3),
                             "picks": [f"{c['algorithm']}/{c['protocol']}/NC{c['num_channels']}/NT"
                                       f"{c['num_threads']}/C{c['chunk_size'] // 1024}K" for c in tuned["configs"]]}},
         "nccl_default_ms": ms_nccl,

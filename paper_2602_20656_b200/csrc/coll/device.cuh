@@ -222,6 +222,7 @@ struct Grp {
   uint64_t* reds = nullptr;       // "reduced": per stage, one arrival per consumer warp
   uint32_t* tiles = nullptr;      // tiles this group has cycled through the ring
   uint32_t* redpar = nullptr;     // producer-private: next parity per stage of `reds`
+  int copy_stage = 0;             // bytes per stage for one-input (copy) steps; 0 = 3 x tile_bytes
   __device__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(n) : "memory"); }
 };
 
@@ -345,10 +346,15 @@ __device__ __noinline__ bool step(const Grp& g, const KParams& P, RecvLink* rl, 
           ln = g.n - 32;
         }
       }
-      const int T = P.tile_bytes, ST = P.tma_stages;
+      // A copy step (one input) owns the stage's three buffers as one tile:
+      // 3x the bytes in flight, which is what bounds a single SM's TMA rate.
+      const int T = NIN == 1 ? (g.copy_stage ? g.copy_stage : 3 * P.tile_bytes) : P.tile_bytes;
+      const int ST = P.tma_stages;
       const int64_t ntiles = (main + T - 1) / T;
       const uint32_t base = *reinterpret_cast<volatile uint32_t*>(g.tiles);
-      auto buf = [&](uint32_t stage, int b) { return g.smem + (static_cast<int64_t>(stage) * 3 + b) * T; };
+      auto buf = [&](uint32_t stage, int b) {
+        return g.smem + (static_cast<int64_t>(stage) * 3 + b) * P.tile_bytes;
+      };
       auto input = [&](int b, int64_t off) -> const char* {
         if (SRC) return b == 0 ? src + off : rs[b > 0 ? b - 1 : 0] + off;
         return rs[b] + off;
@@ -680,10 +686,10 @@ __device__ __forceinline__ void group_copy(const Grp& g, const KParams& P, const
       ln = g.n - 32;
     }
     if (g.tid == 0 && done > 0) {
-      const int T = P.tile_bytes, ST = P.tma_stages;
+      const int T = g.copy_stage ? g.copy_stage : 3 * P.tile_bytes, ST = P.tma_stages;
       const int64_t ntiles = (done + T - 1) / T;
       const uint32_t base = *reinterpret_cast<volatile uint32_t*>(g.tiles);
-      auto buf = [&](uint32_t stage) { return g.smem + static_cast<int64_t>(stage) * 3 * T; };
+      auto buf = [&](uint32_t stage) { return g.smem + static_cast<int64_t>(stage) * T; };
       auto issue = [&](int64_t i) {
         const uint32_t stg = (base + static_cast<uint32_t>(i)) % ST;
         const uint32_t len = static_cast<uint32_t>(lmin(T, done - i * T));
@@ -885,10 +891,11 @@ __device__ void tree_allreduce(const KParams& P, int r, int ch, int nch, volatil
   const Slice sl = channel_slice(N, E, nch, ch);
   if (n == 1) {
     Grp all{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 1, aborts};
-    if (smem) {
+    if (smem) {  // the whole ring (both halves' buffers) for the copy
       all.smem = smem;
       all.bars = bars[0];
       all.tiles = tiles;
+      all.copy_stage = 6 * P.tile_bytes;
     }
     group_copy(all, P, send + sl.lo * E, recv + sl.lo * E, (sl.hi - sl.lo) * E);
     return;
