@@ -149,6 +149,19 @@ int lagom_comm_nvls_import(lagom_comm_t comm, const void* blob);
 int lagom_comm_nvls_bind(lagom_comm_t comm);
 int lagom_comm_nvls_alloc(lagom_comm_t comm, int64_t bytes, void** ptr);
 int64_t lagom_comm_nvls_bytes(lagom_comm_t comm);
+/* One-hop AllToAll through the switch: after nvls_bind, every rank exports
+ * its region's physical allocation (blob), the blobs are all-gathered in rank
+ * order (nranks * LAGOM_HANDLE_BYTES), every rank maps every peer's region,
+ * and all ranks switch it on (nvls_use_peers). Then ALL_TO_ALL with algorithm TREE and recvbuf in the region
+ * stores each block straight into its destination rank's recvbuf (one NVLink
+ * write per byte, no staging). The exporter keeps its fd open until
+ * lagom_comm_destroy, so peers may import at any time before that. */
+int lagom_comm_nvls_export_peer(lagom_comm_t comm, void* blob /* LAGOM_HANDLE_BYTES */);
+int lagom_comm_nvls_import_peers(lagom_comm_t comm, const void* blobs);
+/* Switches the one-hop AllToAll on (1) or off (0). Must be agreed on by all
+ * ranks (call it with the same value everywhere once every rank imported),
+ * since sender and receiver must use the same schedule. */
+int lagom_comm_nvls_use_peers(lagom_comm_t comm, int on);
 
 /* Synthetic data: fills `nelems` elements of `dtype` with uniform values in
  * [-scale, scale) (int32: integers in [-2^20, 2^20)) from a counter-based

@@ -71,6 +71,7 @@ EXPORTED_SYMBOLS = (
     "lagom_coll_launch", "lagom_coll_launch_virtual", "lagom_coll_bytes", "lagom_fill_random",
     "lagom_comm_nvls_supported", "lagom_comm_nvls_export", "lagom_comm_nvls_import",
     "lagom_comm_nvls_bind", "lagom_comm_nvls_alloc", "lagom_comm_nvls_bytes",
+    "lagom_comm_nvls_export_peer", "lagom_comm_nvls_import_peers", "lagom_comm_nvls_use_peers",
 )
 
 _lib = None
@@ -112,6 +113,9 @@ def library() -> ctypes.CDLL:
         "lagom_comm_nvls_bind": (c_int, [vp]),
         "lagom_comm_nvls_alloc": (c_int, [vp, c_i64, ctypes.POINTER(vp)]),
         "lagom_comm_nvls_bytes": (c_i64, [vp]),
+        "lagom_comm_nvls_export_peer": (c_int, [vp, ctypes.c_char_p]),
+        "lagom_comm_nvls_import_peers": (c_int, [vp, ctypes.c_char_p]),
+        "lagom_comm_nvls_use_peers": (c_int, [vp, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -222,6 +226,13 @@ class Communicator:
         dist.barrier(group=group)
         _check(lib.lagom_comm_nvls_bind(self._h), "nvls")
         dist.barrier(group=group)
+        # peer mappings of every rank's region (one-hop AllToAll)
+        _check(lib.lagom_comm_nvls_export_peer(self._h, blob), "nvls")
+        blobs = [None] * self.nranks
+        dist.all_gather_object(blobs, blob.raw, group=group)
+        _check(lib.lagom_comm_nvls_import_peers(self._h, b"".join(blobs)), "nvls")
+        dist.barrier(group=group)
+        _check(lib.lagom_comm_nvls_use_peers(self._h, 1), "nvls")
 
     def nvls_alloc(self, nbytes: int) -> int:
         """Device pointer into the NVLS region (same offset on every rank when
@@ -233,7 +244,7 @@ class Communicator:
     def nvls_tensor(self, numel: int, dtype):
         """A torch tensor whose storage is in the NVLS region (no copy)."""
         import torch
-        typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<u2", torch.float16: "<f2",
+        typestr = {torch.uint8: "|u1", torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<u2", torch.float16: "<f2",
                    torch.int16: "<i2", torch.uint16: "<u2"}[dtype]
         esize = torch.empty(0, dtype=dtype).element_size()
         ptr = self.nvls_alloc(max(16, numel * esize))

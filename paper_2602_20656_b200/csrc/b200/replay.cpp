@@ -419,6 +419,19 @@ struct ReplayEngine::Impl {
       }
       if (ok) ok = agree(lagom_comm_nvls_bind(lcomm) == LAGOM_OK);
       nvls_on = ok;
+      if (ok) {  // peer mappings: one-hop AllToAll (TREE) into the peers' recv buffers
+        unsigned char mine[LAGOM_HANDLE_BYTES];
+        bool pok = agree(lagom_comm_nvls_export_peer(lcomm, mine) == LAGOM_OK);
+        if (pok) {
+          std::vector<unsigned char> all(static_cast<std::size_t>(n) * LAGOM_HANDLE_BYTES);
+          coord.allgather(mine, LAGOM_HANDLE_BYTES, all.data());
+          pok = agree(lagom_comm_nvls_import_peers(lcomm, all.data()) == LAGOM_OK);
+        }
+        if (pok) coll_check(lagom_comm_nvls_use_peers(lcomm, 1), "nvls peers");
+        if (!pok && rank == 0 && trace_on())
+          std::fprintf(stderr, "[lagom] NVLS peer mappings unavailable (%s); AllToAll stays staged\n",
+                       lagom_last_error());
+      }
       if (!ok && rank == 0 && trace_on())
         std::fprintf(stderr, "[lagom] NVLS unavailable (%s); TREE uses the P2P kernels\n", lagom_last_error());
     }

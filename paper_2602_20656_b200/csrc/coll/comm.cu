@@ -96,7 +96,7 @@ int elem_bytes_of(int dtype) {
 }  // namespace
 const void* lagom_pick_simple(int kind, int dtype, int op);
 int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
-                       const void** kernel, void* params_out, size_t* params_bytes);
+                       const void** kernel, void* params_out, size_t* params_bytes, int* smem_bytes);
 void lagom_nvls_release(lagom_comm* c);
 const void* lagom_pick_ll(int kind, int dtype, int op);
 const void* lagom_pick_ll128(int kind, int dtype, int op);
@@ -365,10 +365,11 @@ int lagom_coll_launch(lagom_comm_t c, const lagom_coll_args_t* a, const void* se
     alignas(16) unsigned char nv[512];
     size_t nv_bytes = 0;
     const void* nk = nullptr;
-    if (lagom_nvls_prepare(c, a, sendbuf, recvbuf, &nk, nv, &nv_bytes) == 1) {
+    int nsmem = 0;
+    if (lagom_nvls_prepare(c, a, sendbuf, recvbuf, &nk, nv, &nv_bytes, &nsmem) == 1) {
       void* nargs[] = {nv};
-      LAGOM_CUDA(cudaLaunchKernel(nk, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), nargs, 0,
-                                  static_cast<cudaStream_t>(stream)));
+      LAGOM_CUDA(cudaLaunchKernel(nk, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), nargs,
+                                  static_cast<size_t>(nsmem), static_cast<cudaStream_t>(stream)));
       return LAGOM_OK;
     }
   }

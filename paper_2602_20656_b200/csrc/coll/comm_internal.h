@@ -32,6 +32,12 @@ struct lagom_comm {
   bool nvls_ready = false;
   int64_t off_nvbar = 0, off_nvep = 0;      // NVLS barrier flags / epochs in the heap
   int nvls_export_fd = -1;                  // rank 0's exported fd, closed once bound
+  // Peer (unicast) mappings of every rank's region: one-hop AllToAll writes
+  // straight into the destination rank's recv buffer.
+  char* nvls_peer[LAGOM_MAX_RANKS] = {};    // own entry = nvls_uc
+  bool nvls_peers_mapped = false;          // every peer region mapped here
+  bool nvls_peers_ready = false;           // ... and agreed on by all ranks (use_peers)
+  int nvls_peer_fd = -1;                    // this rank's exported physical-memory fd
 };
 
 // Records `what` as lagom_last_error() and returns `status`.

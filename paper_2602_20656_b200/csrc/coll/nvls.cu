@@ -44,6 +44,7 @@ void* driver_sym(const char* name) {
 
 
 constexpr uint64_t kBlobMagic = 0x4c41474f4d4e564cull;  // "LAGOMNVL"
+constexpr uint64_t kPeerMagic = 0x4c41474f4d504552ull;  // "LAGOMPER"
 struct Blob {
   uint64_t magic;
   int64_t pid;
@@ -91,6 +92,7 @@ struct NvlsParams {
   unsigned int* abort_flag;
   uint64_t timeout_ns;
   unsigned long long* span;
+  char* peer_recv[LAGOM_MAX_RANKS];  // A2A: recv in every rank's region (peer mappings)
 };
 
 __device__ bool nv_wait(const uint64_t* p, uint64_t v, const NvlsParams& P) {
@@ -178,13 +180,37 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
   if (!s_ok) return;
 
   // 16 B units: AR/RS reduce the whole buffer / own block through the switch,
-  // AG broadcasts the own block. Channel c owns a contiguous slice; in AR
-  // each rank further takes 1/n of it (its stores reach every rank).
+  // AG broadcasts the own block, A2A (KIND 3) writes block p straight into
+  // rank p's recv. Channel c owns a contiguous slice; in AR each rank further
+  // takes 1/n of it (its stores reach every rank).
   const int64_t E = P.elem_bytes;
   const int64_t B = P.count;  // elements per block (AR: the whole buffer)
   const int64_t units = B * E / 16;
   const int64_t per_ch = (units + nch - 1) / nch;
   int64_t lo = lagom_dev::lmin(units, per_ch * ch), hi = lagom_dev::lmin(units, per_ch * (ch + 1));
+  const int64_t nt = blockDim.x;
+  if constexpr (KIND == 3) {
+    // One hop through the switch: step k sends block r+k to rank r+k, so at
+    // every step the ranks' destinations form a permutation (no receiver is
+    // the target of two senders at once); k = 0 is the local block.
+    for (int k = 0; k < n; ++k) {
+      const int p = (r + k) % n;
+      const char* in = P.send_uc + static_cast<int64_t>(p) * units * 16;
+      char* out = P.peer_recv[p] + static_cast<int64_t>(r) * units * 16;
+      int64_t u0 = lo + threadIdx.x;
+      for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+        const char* src = in + u0 * 16;
+        char* dst = out + u0 * 16;
+        uint4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) v[j] = *reinterpret_cast<const uint4*>(src + j * nt * 16);
+#pragma unroll
+        for (int j = 0; j < U; ++j) *reinterpret_cast<uint4*>(dst + j * nt * 16) = v[j];
+      }
+      for (; u0 < hi; u0 += nt)
+        *reinterpret_cast<uint4*>(out + u0 * 16) = *reinterpret_cast<const uint4*>(in + u0 * 16);
+    }
+  } else {
   if (KIND == 0) {  // AR: my 1/n share of the channel slice
     const int64_t len = hi - lo, per_r = (len + n - 1) / n;
     const int64_t a = lo + lagom_dev::lmin(len, per_r * r), b = lo + lagom_dev::lmin(len, per_r * (r + 1));
@@ -195,7 +221,6 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
   const int64_t blk = KIND == 0 ? 0 : static_cast<int64_t>(r) * units;  // block offset in units
   // Pointers are advanced per batch so the unrolled body needs no 64-bit
   // index math or bounds checks (keeps U = 16 free of spills at 640 threads).
-  const int64_t nt = blockDim.x;
   const char* in = KIND == 1 ? P.send_uc : P.send_mc + blk * 16;
   char* out = KIND == 2 ? P.recv_uc : P.recv_mc + blk * 16;
   auto load = [&](const char* p) -> uint4 {
@@ -217,10 +242,85 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
     for (int k = 0; k < U; ++k) store(dst + k * nt * 16, v[k]);
   }
   for (; u0 < hi; u0 += nt) store(out + u0 * 16, load(in + u0 * 16));
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();  // my multimem stores are visible everywhere
+    __threadfence_system();  // my multimem / peer stores are visible everywhere
     const bool ok = nv_barrier(P, ch, ep + 1);  // nobody reads results / reuses inputs early
+    if (ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+  }
+}
+
+// One-hop AllToAll through the TMA engine: thread 0 streams every (peer,
+// tile) of the channel slice through a ring of kA2aStages smem stages — bulk
+// load from the local send block, bulk store into the destination rank's recv
+// (one NVLink write per byte). A single SM's TMA engine pushes ~50 GB/s to a
+// peer against ~35 GB/s for 640 threads of vector ld/st (tools/tma_probe.cu),
+// and the rate does not depend on NT.
+constexpr int kA2aStages = 4;
+constexpr int kA2aTile = 48 * 1024;
+constexpr int kA2aSmem = kA2aStages * kA2aTile;
+
+__global__ void __launch_bounds__(640) a2a_tma_kernel(const __grid_constant__ NvlsParams P) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ uint64_t full[kA2aStages];
+  __shared__ int s_ok;
+  const int ch = blockIdx.x, nch = gridDim.x, n = P.nranks, r = P.rank;
+  if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
+  uint64_t* ep_home = reinterpret_cast<uint64_t*>(P.heap[r] + P.off_nvep + static_cast<int64_t>(ch) * 8);
+  const uint64_t ep = *reinterpret_cast<volatile uint64_t*>(ep_home) + 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kA2aStages; ++s) lagom_dev::mbar_init(&full[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_ok = nv_barrier(P, ch, ep) ? 1 : 0;  // every rank's recv is free
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  if (threadIdx.x == 0) {
+    const int64_t blk = P.count * P.elem_bytes;  // bytes per block (16 B multiple)
+    const int64_t units = blk / 16, per_ch = (units + nch - 1) / nch;
+    const int64_t lo = lagom_dev::lmin(units, per_ch * ch) * 16, hi = lagom_dev::lmin(units, per_ch * (ch + 1)) * 16;
+    const int64_t per_peer = (hi - lo + kA2aTile - 1) / kA2aTile, ntiles = per_peer * n;
+    // tile i: step k = i / per_peer sends block r+k to rank r+k (a permutation
+    // of destinations at every step; k = 0 is the local block)
+    auto src_of = [&](int64_t i, uint32_t* len) -> const char* {
+      const int p = static_cast<int>((r + i / per_peer) % n);
+      const int64_t off = lo + (i % per_peer) * kA2aTile;
+      *len = static_cast<uint32_t>(lagom_dev::lmin(kA2aTile, hi - off));
+      return P.send_uc + p * blk + off;
+    };
+    auto dst_of = [&](int64_t i) -> char* {
+      const int p = static_cast<int>((r + i / per_peer) % n);
+      return P.peer_recv[p] + r * blk + lo + (i % per_peer) * kA2aTile;
+    };
+    auto issue = [&](int64_t i) {
+      uint32_t len;
+      const char* src = src_of(i, &len);
+      const int st = static_cast<int>(i % kA2aStages);
+      lagom_dev::mbar_expect(&full[st], len);
+      lagom_dev::bulk_load(ring + st * kA2aTile, src, len, &full[st]);
+    };
+    for (int64_t i = 0; i < ntiles && i < kA2aStages; ++i) issue(i);
+    for (int64_t i = 0; i < ntiles; ++i) {
+      const int st = static_cast<int>(i % kA2aStages);
+      lagom_dev::mbar_wait(&full[st], static_cast<uint32_t>((i / kA2aStages) & 1));
+      uint32_t len;
+      src_of(i, &len);
+      lagom_dev::bulk_store(dst_of(i), ring + st * kA2aTile, len);
+      lagom_dev::bulk_commit();
+      if (i >= 1 && i - 1 + kA2aStages < ntiles) {
+        lagom_dev::bulk_wait_read1();  // tile i-1's store has read its stage
+        issue(i - 1 + kA2aStages);
+      }
+    }
+    lagom_dev::bulk_wait_all();        // every bulk store performed
+    lagom_dev::fence_proxy_global();   // async-proxy writes -> generic proxy
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const bool ok = nv_barrier(P, ch, ep + 1);  // every peer's writes into my recv landed
     if (ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
     if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
   }
@@ -257,7 +357,7 @@ const void* pick_nvls(int dtype, int nt) {
     case 16: return pick_nvls_u<KIND, 16, 640>(dtype);
   }
   if (nt <= 256) return pick_nvls_u<KIND, 32, 256>(dtype);
-  return KIND == 1 ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
+  return (KIND == 1 || KIND == 3) ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
 }
 
 bool inside(const lagom_comm* c, const void* p, int64_t bytes) {
@@ -271,8 +371,18 @@ int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 :
 
 // Used by lagom_coll_launch: 1 if this launch can run on the switch, with
 // *kernel/params filled in; 0 to fall back to the P2P kernels.
+// LAGOM_A2A_TMA=0 selects the LSU (vector ld/st) one-hop AllToAll.
+bool a2a_use_tma() {
+  static const bool on = [] {
+    const char* e = std::getenv("LAGOM_A2A_TMA");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
-                       const void** kernel, void* params_out, size_t* params_bytes) {
+                       const void** kernel, void* params_out, size_t* params_bytes, int* smem_bytes) {
+  *smem_bytes = 0;
   if (!c->nvls_ready || a->algorithm != LAGOM_TREE || a->redop != LAGOM_SUM || c->virt) return 0;
   const int64_t e = ebytes(a->dtype), n = c->nranks;
   int64_t in_b = 0, out_b = 0;
@@ -281,10 +391,26 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
     case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype, a->num_threads); break;
     case LAGOM_ALL_GATHER: in_b = a->count * e; out_b = a->count * e * n; k = pick_nvls<1>(a->dtype, a->num_threads); break;
     case LAGOM_REDUCE_SCATTER: in_b = a->count * e * n; out_b = a->count * e; k = pick_nvls<2>(a->dtype, a->num_threads); break;
+    case LAGOM_ALL_TO_ALL:
+      if (!c->nvls_peers_ready) return 0;
+      in_b = out_b = a->count * e * n;
+      if (a2a_use_tma()) {
+        static const bool smem_ok =
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(&a2a_tma_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
+        if (smem_ok) {
+          k = reinterpret_cast<const void*>(&a2a_tma_kernel);
+          *smem_bytes = kA2aSmem;
+          break;
+        }
+      }
+      k = pick_nvls<3>(a->dtype, a->num_threads);
+      break;
     default: return 0;
   }
   if ((a->count * e) % 16 != 0) return 0;  // whole 16 B units per block
-  const bool send_mc = a->collective != LAGOM_ALL_GATHER, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
+  const bool a2a = a->collective == LAGOM_ALL_TO_ALL;
+  const bool send_mc = a->collective != LAGOM_ALL_GATHER && !a2a, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
   if ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15) return 0;
   if (send_mc && !inside(c, send, in_b)) return 0;
   if (recv_mc && !inside(c, recv, out_b)) return 0;
@@ -297,7 +423,9 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   p.send_uc = static_cast<const char*>(send);
   p.recv_uc = static_cast<char*>(recv);
   p.send_mc = send_mc ? c->nvls_mc + (static_cast<const char*>(send) - c->nvls_uc) : nullptr;
-  p.recv_mc = recv_mc ? c->nvls_mc + (static_cast<char*>(recv) - c->nvls_uc) : nullptr;
+  p.recv_mc = recv_mc && !a2a ? c->nvls_mc + (static_cast<char*>(recv) - c->nvls_uc) : nullptr;
+  if (a2a)
+    for (int q = 0; q < c->nranks; ++q) p.peer_recv[q] = c->nvls_peer[q] + (static_cast<char*>(recv) - c->nvls_uc);
   p.off_nvbar = c->off_nvbar;
   p.off_nvep = c->off_nvep;
   p.abort_flag = c->abort_dev;
@@ -421,10 +549,86 @@ int lagom_comm_nvls_alloc(lagom_comm_t c, int64_t bytes, void** ptr) {
 
 int64_t lagom_comm_nvls_bytes(lagom_comm_t c) { return c && c->nvls_ready ? c->nvls_bytes : 0; }
 
+int lagom_comm_nvls_export_peer(lagom_comm_t c, void* blob) {
+  if (!c || !blob) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_export_peer: bad arguments");
+  if (!c->nvls_ready) return lagom_fail(LAGOM_ERR_NOT_READY, "nvls_export_peer before nvls_bind");
+  std::memset(blob, 0, LAGOM_HANDLE_BYTES);
+  cudaSetDevice(c->device);
+  if (c->nvls_peer_fd < 0) {
+    int fd = -1;
+    LAGOM_DRV(DRV(cuMemExportToShareableHandle)(&fd, static_cast<CUmemGenericAllocationHandle>(c->nvls_mem_handle),
+                                                CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    c->nvls_peer_fd = fd;
+  }
+  Blob b{kPeerMagic, static_cast<int64_t>(getpid()), c->nvls_peer_fd, c->nvls_bytes};
+  std::memcpy(blob, &b, sizeof b);
+  return LAGOM_OK;
+}
+
+int lagom_comm_nvls_import_peers(lagom_comm_t c, const void* blobs) {
+  if (!c || !blobs) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_import_peers: bad arguments");
+  if (!c->nvls_ready) return lagom_fail(LAGOM_ERR_NOT_READY, "nvls_import_peers before nvls_bind");
+  cudaSetDevice(c->device);
+  const size_t g = granularity(c->nranks);
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      c->nvls_peer[q] = c->nvls_uc;
+      continue;
+    }
+    if (c->nvls_peer[q]) continue;
+    Blob b;
+    std::memcpy(&b, static_cast<const unsigned char*>(blobs) + static_cast<size_t>(q) * LAGOM_HANDLE_BYTES, sizeof b);
+    if (b.magic != kPeerMagic || b.size != c->nvls_bytes)
+      return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_import_peers: blob of rank " + std::to_string(q));
+    const int pidfd = static_cast<int>(syscall(SYS_pidfd_open, static_cast<pid_t>(b.pid), 0));
+    if (pidfd < 0) return lagom_fail(LAGOM_ERR_CUDA, "pidfd_open failed");
+    const int fd = static_cast<int>(syscall(SYS_pidfd_getfd, pidfd, static_cast<int>(b.fd), 0));
+    close(pidfd);
+    if (fd < 0) return lagom_fail(LAGOM_ERR_CUDA, "pidfd_getfd failed (ptrace permission?)");
+    CUmemGenericAllocationHandle h;
+    const CUresult r = DRV(cuMemImportFromShareableHandle)(&h, reinterpret_cast<void*>(static_cast<intptr_t>(fd)),
+                                                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(fd);
+    if (r != CUDA_SUCCESS) return drv_fail(r, "cuMemImportFromShareableHandle (peer)");
+    CUdeviceptr va = 0;
+    CUresult m = DRV(cuMemAddressReserve)(&va, static_cast<size_t>(b.size), g, 0, 0);
+    if (m == CUDA_SUCCESS) m = DRV(cuMemMap)(va, static_cast<size_t>(b.size), 0, h, 0);
+    DRV(cuMemRelease)(h);  // the mapping holds its own reference
+    if (m == CUDA_SUCCESS) m = DRV(cuMemSetAccess)(va, static_cast<size_t>(b.size), &acc, 1);
+    if (m != CUDA_SUCCESS) return drv_fail(m, "map peer NVLS region");
+    c->nvls_peer[q] = reinterpret_cast<char*>(va);
+  }
+  c->nvls_peers_mapped = true;
+  return LAGOM_OK;
+}
+
+int lagom_comm_nvls_use_peers(lagom_comm_t c, int on) {
+  if (!c) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_use_peers: null comm");
+  if (on && !c->nvls_peers_mapped) return lagom_fail(LAGOM_ERR_NOT_READY, "nvls_use_peers before import_peers");
+  c->nvls_peers_ready = on != 0;
+  return LAGOM_OK;
+}
+
 }  // extern "C"
 
 void lagom_nvls_release(lagom_comm* c) {
   if (!c) return;
+  for (int q = 0; q < LAGOM_MAX_RANKS; ++q) {
+    if (c->nvls_peer[q] && q != c->rank) {
+      DRV(cuMemUnmap)(reinterpret_cast<CUdeviceptr>(c->nvls_peer[q]), static_cast<size_t>(c->nvls_bytes));
+      DRV(cuMemAddressFree)(reinterpret_cast<CUdeviceptr>(c->nvls_peer[q]), static_cast<size_t>(c->nvls_bytes));
+    }
+    c->nvls_peer[q] = nullptr;
+  }
+  c->nvls_peers_ready = c->nvls_peers_mapped = false;
+  if (c->nvls_peer_fd >= 0) {
+    close(c->nvls_peer_fd);
+    c->nvls_peer_fd = -1;
+  }
   if (c->nvls_export_fd >= 0) {
     close(c->nvls_export_fd);
     c->nvls_export_fd = -1;

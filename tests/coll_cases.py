@@ -10,6 +10,10 @@ from paper_2602_20656_b200 import coll as C
 # (collective, algorithm) pairs of the kernel family
 FAMILY = [(C.ALL_REDUCE, C.RING), (C.ALL_REDUCE, C.TREE), (C.ALL_GATHER, C.RING),
           (C.REDUCE_SCATTER, C.RING), (C.ALL_TO_ALL, C.RING)]
+# TREE keys of the other collectives: in-switch (NVLS) AllGather/ReduceScatter
+# and the one-hop AllToAll when the buffers live in an NVLS region; elsewhere
+# they run the ring schedule.
+TREE_EXTRA = [(C.ALL_GATHER, C.TREE), (C.REDUCE_SCATTER, C.TREE), (C.ALL_TO_ALL, C.TREE)]
 PROTOS = [C.SIMPLE, C.LL, C.LL128]
 NAMES = {0: "AR", 1: "AG", 2: "RS", 3: "A2A"}
 DT_NAMES = {0: "f32", 1: "bf16", 2: "f16", 3: "i32"}
@@ -21,10 +25,10 @@ CONFIGS = [(1, 64, 1024), (2, 128, 4096), (3, 192, 32768), (5, 320, 8192),
 COUNTS = [1, 7, 100, 1000, 4099, 65536 + 3, 300000]
 
 
-def cases(nranks_list, seed=0, per_combo=2):
+def cases(nranks_list, seed=0, per_combo=2, tree_extra=False):
     rng = np.random.default_rng(seed)
     out = []
-    for (coll, algo), proto in itertools.product(FAMILY, PROTOS):
+    for (coll, algo), proto in itertools.product(FAMILY + (TREE_EXTRA if tree_extra else []), PROTOS):
         for n in nranks_list:
             for dtype in (0, 1, 3) + ((2,) if coll == C.ALL_REDUCE else ()):
                 for _ in range(per_combo):

@@ -13,13 +13,7 @@ import torch.distributed as dist  # noqa: E402
 
 from paper_2602_20656_b200 import coll as C  # noqa: E402
 from tests import coll_cases  # noqa: E402
-from tests.oracle_ref import collective as oracle_collective, out_elems  # noqa: E402
-
-
-def nvls_tensor(comm, t):
-    out = comm.nvls_tensor(t.numel(), t.dtype)
-    out.copy_(t)
-    return out
+from tests.oracle_ref import collective as oracle_collective, in_elems, out_elems  # noqa: E402
 
 
 def within_tolerance(got, want, sends, c):
@@ -48,8 +42,9 @@ def main():
     nvls = bool(os.environ.get("LAGOM_NVLS")) and comm.nvls_supported()
     if nvls:
         comm.enable_nvls(1 << 30)
-    fails = 0
-    cases = coll_cases.cases([world], seed=int(os.environ.get("LAGOM_CASE_SEED", "99")), per_combo=2)
+    fails, checked = 0, 0
+    cases = coll_cases.cases([world], seed=int(os.environ.get("LAGOM_CASE_SEED", "99")), per_combo=2,
+                             tree_extra=True)
     for c in cases:
         c["nc"] = max(1, min(32, c["nc"] * 2))  # real mode: no co-residency cap
     if os.environ.get("LAGOM_BIG"):
@@ -60,31 +55,54 @@ def main():
                      (coll, dt, nc, ch, cnt) for coll in (C.ALL_REDUCE, C.REDUCE_SCATTER, C.ALL_GATHER)
                      for dt in (0, 1) for nc in (8, 32) for ch in (1 << 20, 4 << 20)
                      for cnt in (3 << 20, (8 << 20) + 5))]
+        # TREE keys: in-switch AG/RS and the one-hop AllToAll (NVLS region)
+        cases += [dict(coll=coll, algo=C.TREE, proto=0, n=world, dtype=dt, op=0, nc=nc, nt=nt, chunk=1 << 20,
+                       count=cnt, seed=2000 + i)
+                  for i, (coll, dt, nc, nt, cnt) in enumerate(
+                      (coll, dt, nc, nt, cnt) for coll in (C.ALL_TO_ALL, C.ALL_GATHER, C.REDUCE_SCATTER)
+                      for dt in (1, 3) for nc, nt in ((4, 256), (8, 640)) for cnt in (1 << 20, (2 << 20) + 8))]
+    # Buffers inside the multicast region are carved once (same offsets on
+    # every rank) and reused by every case: the region is a bump allocator.
+    # A canary band after the output catches writes past its end.
+    band = 4096
+    nbytes = max(4 * max(in_elems(c["coll"], world, c["count"]), out_elems(c["coll"], world, c["count"]))
+                 for c in cases) + band
+    if nvls:
+        xbuf = comm.nvls_tensor(nbytes, torch.uint8)
+        ybuf = comm.nvls_tensor(nbytes, torch.uint8)
+    else:
+        xbuf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        ybuf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    for c in cases:
         sends = coll_cases.inputs(c)
         want = oracle_collective(c["coll"], c["algo"], c["dtype"], c["op"], sends)[rank]
-        x = torch.from_numpy(sends[rank]).cuda()
-        y = torch.empty(out_elems(c["coll"], world, c["count"]), dtype=x.dtype, device="cuda")
-        if nvls:  # buffers inside the multicast region (same offsets on every rank)
-            x = nvls_tensor(comm, x)
-            y = nvls_tensor(comm, y)
-        y.view(torch.uint8).fill_(0xAB)
+        xs = torch.from_numpy(sends[rank].view(np.uint8).copy()).cuda()
+        xbuf[:xs.numel()].copy_(xs)
+        out_b = want.nbytes
+        ybuf[:out_b + band].fill_(0xAB)
         cfg = C.CollConfig(c["algo"], c["proto"], c["nc"], c["nt"], c["chunk"])
-        comm.launch(c["coll"], cfg, c["dtype"], c["count"], x.data_ptr(), y.data_ptr(), stream, c["op"])
+        comm.launch(c["coll"], cfg, c["dtype"], c["count"], xbuf.data_ptr(), ybuf.data_ptr(), stream, c["op"])
         torch.cuda.synchronize()
         comm.check()
-        got = y.cpu().numpy()
-        exact = not (nvls and c["algo"] == C.TREE and c["dtype"] != C.I32 and c["coll"] != C.ALL_GATHER)
+        got = ybuf[:out_b].cpu().numpy().view(want.dtype)
+        canary_ok = bool((ybuf[out_b:out_b + band] == 0xAB).all())
+        exact = not (nvls and c["algo"] == C.TREE and c["dtype"] != C.I32
+                     and c["coll"] in (C.ALL_REDUCE, C.REDUCE_SCATTER))
         if not exact:  # switch-side fp32 accumulation: stated tolerance, not bits
             ok = within_tolerance(got, want, sends, c)
         else:
             ok = got.tobytes() == want.tobytes()
+        ok = ok and canary_ok
+        checked += 1
         if not ok:
             fails += 1
-            print(f"[rank {rank}] MISMATCH {coll_cases.case_id(c)}", flush=True)
+            print(f"[rank {rank}] MISMATCH {coll_cases.case_id(c)} canary_ok={canary_ok}", flush=True)
     t = torch.tensor([fails])
     dist.all_reduce(t)
     if rank == 0:
-        print(f"mp_coll_check: world={world} cases={len(cases)} failing(sum over ranks)={int(t)}", flush=True)
+        print(f"mp_coll_check: world={world} nvls={int(nvls)} cases={len(cases)} checked={checked} "
+              f"failing(sum over ranks)={int(t)}", flush=True)
+    assert checked == len(cases)
     comm.close()
     dist.destroy_process_group()
     sys.exit(min(int(t), 100))
