@@ -244,7 +244,7 @@ def main():
         t_tune = time.perf_counter()
         eng.run_compute_only()  # first-touch / clocks settle before the search
         starts = ["min", "nccl-default"] if args.start == "best" else [args.start]
-        eng.set_measurement(3, 1)  # each profile call: median of 3 replays after 1 warmup
+        eng.set_measurement(5, 2)  # each profile call: median of 5 replays after 2 warmups
         params_doc = open(args.params).read() if args.params and os.path.exists(args.params) else ""
         if params_doc:
             pj = json.loads(params_doc)
@@ -256,8 +256,9 @@ def main():
         # assignments are compared head to head (interleaved) before choosing.
         docs = {st: json.dumps({"configs": [r["configs"][g] for g in groups]}) for st, r in runs.items()}
         zsel = {st: [] for st in runs}
-        for _ in range(3 if len(runs) > 1 else 0):
-            for st in runs:
+        order = list(runs)
+        for i in range(6 if len(runs) > 1 else 0):  # alternating order, so neither keeps a predecessor
+            for st in (order if i % 2 == 0 else order[::-1]):
                 zsel[st].append(json.loads(eng.run(docs[st]))["Z"])
         best_start = min(runs, key=lambda st: statistics.median(zsel[st]) if zsel[st] else 0.0)
         tune_runs = runs

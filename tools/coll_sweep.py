@@ -65,11 +65,15 @@ def main():
     comm = C.Communicator.from_process_group(device=local, max_channels=64, use_tma=args.use_tma)
     stream = torch.cuda.current_stream()
     s_ptr = stream.cuda_stream
+    sizes = [parse_size(s) for s in args.sizes.split(",")]
     if args.nvls:
-        comm.enable_nvls(6 << 30)
+        # the region is a bump allocator: carve the largest send/recv once and reuse views
+        big = max(sizes) * world + 4096
+        comm.enable_nvls(2 * big + (64 << 20))
+        xbig, ybig = comm.nvls_tensor(big, torch.uint8), comm.nvls_tensor(big, torch.uint8)
     names = {"AR": C.ALL_REDUCE, "AG": C.ALL_GATHER, "RS": C.REDUCE_SCATTER, "A2A": C.ALL_TO_ALL}
     rows = []
-    for size in [parse_size(s) for s in args.sizes.split(",")]:
+    for size in sizes:
         for cn in args.colls.split(","):
             coll = names[cn]
             # size = algorithmic bytes S (nccl-tests): AR buffer; AG/RS/A2A total
@@ -79,7 +83,8 @@ def main():
             x = torch.randn(n_in, device="cuda", dtype=torch.bfloat16)
             y = torch.empty(n_out, device="cuda", dtype=torch.bfloat16)
             if args.nvls:
-                xn, y = comm.nvls_tensor(n_in, torch.bfloat16), comm.nvls_tensor(n_out, torch.bfloat16)
+                xn = xbig[:2 * n_in].view(torch.bfloat16)
+                y = ybig[:2 * n_out].view(torch.bfloat16)
                 xn.copy_(x)
                 x = xn
             s_bytes, fac = C.coll_bytes(coll, C.BF16, count, world)

@@ -35,11 +35,33 @@ KIB = 1024
 MIB = 1 << 20
 
 
-def dag_for(sizes_mib, gemm):
-    comm = [{"id": f"ar{s}", "collective": "ALL_REDUCE", "dtype": 1, "count": s * MIB // 2,
-             "ready_after": None, "role": i} for i, s in enumerate(sizes_mib)]
+COLLS = ("ALL_REDUCE", "ALL_GATHER", "REDUCE_SCATTER", "ALL_TO_ALL")
+
+
+def dag_for(sizes_mib, gemm, nranks):
+    """Comm ops: every collective at every size (message_bytes = s MiB: the
+    AR buffer, the AG output, the RS input, the A2A send), AllReduce first."""
+    comm = []
+    for coll in COLLS:
+        for s in sizes_mib:
+            count = s * MIB // 2 // (1 if coll == "ALL_REDUCE" else nranks)
+            comm.append({"id": f"{coll.lower()}{s}", "collective": coll, "dtype": 1, "count": count,
+                         "ready_after": None, "role": len(comm)})
     return {"name": "contention-probe", "compute_ops": [{"id": "victim", "gemms": [gemm] * 8}],
             "comm_ops": comm}
+
+
+def fit_factor(co, link, pts):
+    """The reference's collective_factors (default_params.json:164-169) scale
+    message bytes inside comm_time; fit one factor per collective against the
+    subspace's AllReduce-fitted coefficients (median relative error)."""
+    best = None
+    for f in np.geomspace(0.2, 5.0, 241):
+        rel = [abs(predict(co, link, nc, nt, c, m * f) - x) / x for nc, nt, c, m, x in pts]
+        err = float(np.median(rel))
+        if best is None or err < best[0]:
+            best = (err, float(f), float(np.percentile(rel, 90)))
+    return best
 
 
 def cfg(algo, proto, nc, nt, c):
@@ -79,12 +101,86 @@ def predict(co, link, nc, nt, c, m):
         m / min(nc * co["per_channel_bw"] * eta, link)
 
 
+def fit_all(meas, meas_coll, over, y0, lam):
+    """Fits the reference cost model's coefficients from the measurements
+    (median-relative-error least squares, tools/predict_vs_measured.fit)."""
+    from tools.predict_vs_measured import fit as fit_model
+    params, report = {}, {}
+    for key, pts in meas.items():
+        co, link, rep = fit_model(pts)
+        co.update({"mem_coeff": 0.5, "chunk_knee": 128 * KIB})
+        params[key] = co
+        report[key] = dict(rep, link_bw=link)
+    # victim: SM loss lambda/(lambda-NC) explains part of the slowdown; the
+    # remainder is attributed to the comm's HBM footprint V (wave_time's
+    # blocks*D/(B - V) term) -> kappa, C_knee for RING/SIMPLE.
+    peak = 6434.2e3  # bytes/us, measured copy bandwidth (MEASURED_PEAKS.json)
+    rows = []
+    for nc, c, y, _ in over:
+        sm_part = y0 * lam / (lam - nc)
+        rows.append((nc, c, max(0.0, y / sm_part - 1.0)))
+    best = None
+    for knee in [32 * KIB, 64 * KIB, 128 * KIB, 256 * KIB, 512 * KIB, 1 * MIB]:
+        X = np.array([[nc * c / (c + knee)] for nc, c, _ in rows])
+        Y = np.array([e for *_, e in rows])
+        k, *_ = np.linalg.lstsq(X, Y, rcond=None)
+        err = float(np.sum((X @ k - Y) ** 2))
+        if best is None or err < best[0]:
+            best = (err, knee, float(k[0]))
+    _, knee, slope = best
+    # slope ~ V/(B - V) per (NC*sat) ~= kappa*b_chan/B for V << B
+    b_chan = params["RING/SIMPLE/P2P"]["per_channel_bw"]
+    params["RING/SIMPLE/P2P"]["mem_coeff"] = max(0.0, slope * peak / b_chan)
+    params["RING/SIMPLE/P2P"]["chunk_knee"] = int(knee)
+    # Per-collective traffic factors, fitted on the TREE key (the subspace
+    # the search selects on an NVSwitch box).
+    factors, factor_report = {"ALL_REDUCE": 2.0}, {}
+    if "TREE/SIMPLE/P2P" in params and meas_coll.get("TREE/SIMPLE/P2P"):
+        co, lk = params["TREE/SIMPLE/P2P"], report["TREE/SIMPLE/P2P"]["link_bw"]
+        for coll, pts in meas_coll["TREE/SIMPLE/P2P"].items():
+            err, f, p90 = fit_factor(co, lk, [tuple(p) for p in pts])
+            factors[coll] = f
+            factor_report[coll] = {"factor": f, "median_rel_err": err, "p90_rel_err": p90, "points": len(pts)}
+    for coll in COLLS[1:]:
+        factors.setdefault(coll, 1.0)
+    params["collective_factors"] = factors
+    gpu = {"num_sms": lam, "peak_mem_bw": peak, "link_bw": max(r["link_bw"] for r in report.values()),
+           "comm_bw_cap_fraction": 0.6, "compute_on_comm_slowdown": 0.0}
+    return params, gpu, report, factor_report
+
+
+def validate(L, gpu, params):
+    """Loads the params document with the product loader (reference schema)."""
+    L.tune_sim(json.dumps({"gpu": gpu, "compute_ops": [{"id": "c", "total_blocks": 1, "blocks_per_sm": 1,
+                                                        "bytes_per_block": 0, "base_wave_time": 1.0}],
+                           "comm_ops": [{"id": "k", "collective": "ALL_REDUCE", "message_bytes": 1 << 20}]}),
+               "min", 5, json.dumps(params))
+
+
+def refit(path, out):
+    """GPU-free: recomputes every fit from a stored profile's measurements."""
+    from paper_2602_20656_b200 import _lagom_py as L
+    prof = json.load(open(path))
+    meas = {k: [tuple(p) for p in v] for k, v in prof["measurements"].items()}
+    params, gpu, report, factor_report = fit_all(meas, prof.get("measurements_other", {}),
+                                                 prof["victim"]["overlapped"], prof["victim"]["y_alone_us"],
+                                                 prof["gpu"]["num_sms"])
+    validate(L, gpu, params)
+    prof.update(params=params, gpu=gpu, fit_report=report, factor_report=factor_report)
+    with open(out, "w") as f:
+        json.dump(prof, f, indent=1)
+    print(json.dumps({"fit_report": report, "factor_report": factor_report}, indent=1))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="profiles/fitted_params.json")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--nvls", type=int, default=1, help="TREE = in-switch (NVLS) when the box supports it")
+    ap.add_argument("--refit", default="", help="recompute the fits of a stored profile (no GPU) into --out")
     a = ap.parse_args()
+    if a.refit:
+        return refit(a.refit, a.out)
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
     import torch
@@ -99,12 +195,19 @@ def main():
         token = tok[0]
     else:
         token = secrets.token_hex(6)
-    sizes = [1, 8, 32] if a.quick else [1, 4, 16, 64]
+    sizes = [1, 8, 32] if a.quick else [1, 4, 16, 64, 256]
     gemm = [8192, 8192, 2048]  # a 275 GFLOP compute-bound victim op (x8 per replay)
-    dag = dag_for(sizes, gemm)
-    eng = L.ReplayEngine(json.dumps(dag), f"lagom_cp_{token}", rank, world, local, repeats=3, warmup=1,
-                         nccl=False, reserve_comm_sms=True, nvls=bool(a.nvls), max_channels=64)
-    if rank != 0:
+    dag = dag_for(sizes, gemm, world)
+    dag_ar = dict(dag, comm_ops=[op for op in dag["comm_ops"] if op["collective"] == "ALL_REDUCE"])
+
+    def engine(d, tag):
+        return L.ReplayEngine(json.dumps(d), f"lagom_cp{tag}_{token}", rank, world, local, repeats=3, warmup=1,
+                              nccl=False, reserve_comm_sms=True, nvls=bool(a.nvls), max_channels=64)
+    eng = engine(dag, "a")
+    if rank != 0:  # serve phase 1 (comm alone), then phase 2 (victim overlapped)
+        eng.serve()
+        eng.close()
+        eng = engine(dag_ar, "b")
         eng.serve()
         eng.close()
         if world > 1:
@@ -116,19 +219,28 @@ def main():
     keys = [("RING", "SIMPLE"), ("RING", "LL"), ("RING", "LL128"), ("TREE", "SIMPLE")]
     if a.quick:
         ncs, nts, chunks, keys = [1, 4, 16], [256, 640], [256 * KIB, 2 * MIB], keys[:2]
-    meas = {}
+    meas, meas_coll = {}, {}
     factor = 2.0  # AllReduce traffic factor (reference collective_factors)
+    nops = len(dag["comm_ops"])
     for (algo, proto) in keys:
-        pts = []
+        pts, other = [], {c: [] for c in COLLS[1:]}
         for nc, nt, c in itertools.product(ncs, nts, chunks):
             if proto == "LL" and c > 1 * MIB:
                 continue
-            r = json.loads(eng.run_comm_only(json.dumps({"configs": [cfg(algo, proto, nc, nt, c)] * len(sizes)})))
-            for s, x in zip(sizes, r["x"]):
-                pts.append((nc, nt, c, s * MIB * factor, x))
+            r = json.loads(eng.run_comm_only(json.dumps({"configs": [cfg(algo, proto, nc, nt, c)] * nops})))
+            for op, x in zip(dag["comm_ops"], r["x"]):
+                s = int(op["id"].lstrip("abcdefghijklmnopqrstuvwxyz_"))
+                if op["collective"] == "ALL_REDUCE":
+                    pts.append((nc, nt, c, s * MIB * factor, x))
+                else:
+                    other[op["collective"]].append((nc, nt, c, s * MIB, x))
         meas[f"{algo}/{proto}/P2P"] = pts
-        print(f"[profile] {algo}/{proto}: {len(pts)} points", flush=True)
-    # victim alone and overlapped
+        meas_coll[f"{algo}/{proto}/P2P"] = other
+        print(f"[profile] {algo}/{proto}: {len(pts)} AllReduce points (+ AG/RS/A2A)", flush=True)
+    eng.stop()
+    eng.close()
+    # victim alone and overlapped (AllReduce ops only)
+    eng = engine(dag_ar, "b")
     y0 = json.loads(eng.run_compute_only())["Y"]
     over = []
     for nc, c in itertools.product([1, 2, 4, 8, 16, 32], [64 * KIB, 1 * MIB, 4 * MIB]):
@@ -137,52 +249,18 @@ def main():
     eng.stop()
     eng.close()
 
-    # ---- fits (median-relative-error least squares, tools/predict_vs_measured.fit)
-    from tools.predict_vs_measured import fit as fit_model
-    params, report = {}, {}
-    for key, pts in meas.items():
-        co, link, rep = fit_model(pts)
-        co.update({"mem_coeff": 0.5, "chunk_knee": 128 * KIB})
-        params[key] = co
-        report[key] = dict(rep, link_bw=link)
-    # victim: SM loss lambda/(lambda-NC) explains part of the slowdown; the
-    # remainder is attributed to the comm's HBM footprint V (wave_time's
-    # blocks*D/(B - V) term) -> kappa, C_knee for RING/SIMPLE.
     lam = torch.cuda.get_device_properties(local).multi_processor_count
-    peak = 6434.2e3  # bytes/us, measured copy bandwidth (MEASURED_PEAKS.json)
-    rows, ys = [], []
-    for nc, c, y, _ in over:
-        sm_part = y0 * lam / (lam - nc)
-        extra = max(0.0, y / sm_part - 1.0)
-        rows.append((nc, c, extra))
-    best = None
-    for knee in [32 * KIB, 64 * KIB, 128 * KIB, 256 * KIB, 512 * KIB, 1 * MIB]:
-        X = np.array([[nc * c / (c + knee)] for nc, c, _ in rows])
-        Y = np.array([e for *_, e in rows])
-        k, *_ = np.linalg.lstsq(X, Y, rcond=None)
-        err = float(np.sum((X @ k - Y) ** 2))
-        if best is None or err < best[0]:
-            best = (err, knee, float(k[0]))
-    _, knee, slope = best
-    # slope ~ V/(B - V) per (NC*sat) ~= kappa*b_chan/B for V << B
-    b_chan = params["RING/SIMPLE/P2P"]["per_channel_bw"]
-    kappa = max(0.0, slope * peak / b_chan)
-    params["RING/SIMPLE/P2P"]["mem_coeff"] = kappa
-    params["RING/SIMPLE/P2P"]["chunk_knee"] = int(knee)
-    params["collective_factors"] = {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0}
-    gpu = {"num_sms": lam, "peak_mem_bw": peak, "link_bw": max(r["link_bw"] for r in report.values()),
-           "comm_bw_cap_fraction": 0.6, "compute_on_comm_slowdown": 0.0}
-    # validate the params document with the product loader (reference schema)
-    L.tune_sim(json.dumps({"gpu": gpu, "compute_ops": [{"id": "c", "total_blocks": 1, "blocks_per_sm": 1,
-                                                        "bytes_per_block": 0, "base_wave_time": 1.0}],
-                           "comm_ops": [{"id": "k", "collective": "ALL_REDUCE", "message_bytes": 1 << 20}]}),
-               "min", 5, json.dumps(params))
-    out = {"nranks": world, "params": params, "gpu": gpu, "fit_report": report,
-           "victim": {"y_alone_us": y0, "overlapped": over}, "measurements": meas}
+    params, gpu, report, factor_report = fit_all(meas, meas_coll, over, y0, lam)
+    from paper_2602_20656_b200 import _lagom_py as L2
+    validate(L2, gpu, params)
+    out = {"nranks": world, "params": params, "gpu": gpu, "fit_report": report, "factor_report": factor_report,
+           "victim": {"y_alone_us": y0, "overlapped": over}, "measurements": meas,
+           "measurements_other": meas_coll}
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
-    print(json.dumps({"fit_report": report, "gpu": gpu, "RING/SIMPLE": params["RING/SIMPLE/P2P"]}), flush=True)
+    print(json.dumps({"fit_report": report, "factor_report": factor_report, "gpu": gpu,
+                      "RING/SIMPLE": params["RING/SIMPLE/P2P"]}), flush=True)
     if world > 1:
         dist.barrier()
 

@@ -34,7 +34,7 @@ def fit(points):
     link_hi = max(p[3] / p[4] for p in points)
     for eta0 in np.linspace(0.05, 1.0, 20):
         for link in link_hi * np.array([0.9, 1.0, 1.1, 1.3, 1.6]):
-            for b in np.geomspace(2e3, 2e5, 50):
+            for b in np.geomspace(2e3, 1e6, 70):  # bytes/us per channel (NVLS channels reach ~2e5)
                 A = np.array([[1.0, p[0], math.ceil(p[3] / (p[0] * p[2]))] for p in points])
                 bw = np.array([min(p[0] * b * (eta0 + (1 - eta0) * p[1] / 640.0), link) for p in points])
                 y = xs - np.array([p[3] for p in points]) / bw
@@ -73,7 +73,8 @@ def main():
     # footprint from the overlapped-victim sweep (reference mem_footprint form)
     params["RING/SIMPLE/P2P"]["mem_coeff"] = prof["params"]["RING/SIMPLE/P2P"]["mem_coeff"]
     params["RING/SIMPLE/P2P"]["chunk_knee"] = prof["params"]["RING/SIMPLE/P2P"]["chunk_knee"]
-    params["collective_factors"] = {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0}
+    params["collective_factors"] = prof["params"].get(
+        "collective_factors", {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0})
 
     bench = json.load(open(a.bench))
     line, raw = bench["line"], bench["raw"]
