@@ -55,6 +55,11 @@ def test_status_strings_and_errors_without_gpu():
     with pytest.raises(C.LagomError) as e:
         C.Communicator(5, 2, 0)  # rank out of range: rejected before touching CUDA
     assert e.value.code == "INVALID_INPUT"
+    # NVLS peer-mapping entry points reject a null communicator without CUDA
+    blob = ctypes.create_string_buffer(64)
+    assert lib.lagom_comm_nvls_export_peer(None, blob) == 1
+    assert lib.lagom_comm_nvls_import_peers(None, blob) == 1
+    assert lib.lagom_comm_nvls_use_peers(None, 1) == 1
 
 
 def test_config_mapping_from_reference_json():
