@@ -210,6 +210,28 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
       for (; u0 < hi; u0 += nt)
         *reinterpret_cast<uint4*>(out + u0 * 16) = *reinterpret_cast<const uint4*>(in + u0 * 16);
     }
+  } else if constexpr (KIND == 4) {
+    // One-hop AllGather (n = 2 default): load the own block once, store it
+    // into every rank's recv (the local copy plus one NVLink write per peer).
+    // A multicast store would also carry the sender's own copy through the
+    // switch, which caps NVLS AllGather at (n-1)/n of the link per GPU.
+    const char* in = P.send_uc;
+    const int64_t at = static_cast<int64_t>(r) * units * 16;
+    int64_t u0 = lo + threadIdx.x;
+    for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = *reinterpret_cast<const uint4*>(in + (u0 + j * nt) * 16);
+      for (int k = 1; k <= n; ++k) {
+        char* out = P.peer_recv[(r + k) % n] + at;
+#pragma unroll
+        for (int j = 0; j < U; ++j) *reinterpret_cast<uint4*>(out + (u0 + j * nt) * 16) = v[j];
+      }
+    }
+    for (; u0 < hi; u0 += nt) {
+      const uint4 v = *reinterpret_cast<const uint4*>(in + u0 * 16);
+      for (int k = 1; k <= n; ++k) *reinterpret_cast<uint4*>(P.peer_recv[(r + k) % n] + at + u0 * 16) = v;
+    }
   } else {
   if (KIND == 0) {  // AR: my 1/n share of the channel slice
     const int64_t len = hi - lo, per_r = (len + n - 1) / n;
@@ -357,7 +379,7 @@ const void* pick_nvls(int dtype, int nt) {
     case 16: return pick_nvls_u<KIND, 16, 640>(dtype);
   }
   if (nt <= 256) return pick_nvls_u<KIND, 32, 256>(dtype);
-  return (KIND == 1 || KIND == 3) ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
+  return (KIND == 1 || KIND == 3 || KIND == 4) ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
 }
 
 bool inside(const lagom_comm* c, const void* p, int64_t bytes) {
@@ -371,6 +393,24 @@ int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 :
 
 // Used by lagom_coll_launch: 1 if this launch can run on the switch, with
 // *kernel/params filled in; 0 to fall back to the P2P kernels.
+// TREE AllGather through peer stores instead of multicast. At n = 2 the
+// multicast echo of the sender's own copy caps NVLS AllGather at ~330 GB/s
+// busbw from NC = 8 upward, while peer stores keep scaling with the channels
+// (4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355 vs 278; NC 32: 569 vs
+// 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl). LAGOM_AG_ONE_HOP=2 follows
+// the config (peer stores at n = 2 and NC >= 12, multicast otherwise; every
+// rank launches the same config, so every rank makes the same choice), 1
+// forces peer stores, 0 / unset keeps multicast. It is off by default: in the
+// FSDP replay at n = 2 the faster AllGather let the search push the
+// ReduceScatter to NC 45-57 and the iteration got slower.
+bool ag_one_hop(int n, int nc) {
+  static const int mode = [] {
+    const char* e = std::getenv("LAGOM_AG_ONE_HOP");
+    return e && *e ? std::atoi(e) : 0;
+  }();
+  return mode == 1 || (mode == 2 && n == 2 && nc >= 12);
+}
+
 // LAGOM_A2A_TMA=0 selects the LSU (vector ld/st) one-hop AllToAll.
 bool a2a_use_tma() {
   static const bool on = [] {
@@ -389,7 +429,12 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   const void* k = nullptr;
   switch (a->collective) {
     case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype, a->num_threads); break;
-    case LAGOM_ALL_GATHER: in_b = a->count * e; out_b = a->count * e * n; k = pick_nvls<1>(a->dtype, a->num_threads); break;
+    case LAGOM_ALL_GATHER:
+      in_b = a->count * e;
+      out_b = a->count * e * n;
+      k = (c->nvls_peers_ready && ag_one_hop(c->nranks, a->num_channels)) ? pick_nvls<4>(a->dtype, a->num_threads)
+                                                         : pick_nvls<1>(a->dtype, a->num_threads);
+      break;
     case LAGOM_REDUCE_SCATTER: in_b = a->count * e * n; out_b = a->count * e; k = pick_nvls<2>(a->dtype, a->num_threads); break;
     case LAGOM_ALL_TO_ALL:
       if (!c->nvls_peers_ready) return 0;
@@ -409,7 +454,9 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
     default: return 0;
   }
   if ((a->count * e) % 16 != 0) return 0;  // whole 16 B units per block
-  const bool a2a = a->collective == LAGOM_ALL_TO_ALL;
+  // peer-store kernels (one-hop AllToAll / AllGather) write into peer_recv
+  const bool a2a = a->collective == LAGOM_ALL_TO_ALL ||
+                   (a->collective == LAGOM_ALL_GATHER && c->nvls_peers_ready && ag_one_hop(c->nranks, a->num_channels));
   const bool send_mc = a->collective != LAGOM_ALL_GATHER && !a2a, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
   if ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15) return 0;
   if (send_mc && !inside(c, send, in_b)) return 0;

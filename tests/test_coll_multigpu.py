@@ -40,3 +40,18 @@ def test_real_multigpu_parity(world, nvls):
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_real_multigpu_parity_one_hop_allgather(world):
+    """TREE AllGather through peer stores (LAGOM_AG_ONE_HOP=1) instead of
+    multicast: bit-exact like every movement collective."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_AG_ONE_HOP="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_coll_check.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
