@@ -31,7 +31,7 @@ CU_SRCS    := $(wildcard $(PKG)/csrc/coll/*.cu)
 CU_OBJS    := $(patsubst $(PKG)/csrc/coll/%.cu,build/coll/%.o,$(CU_SRCS))
 
 .PHONY: all host coll b200 py oracle clean
-all: host coll b200 py cli build/parity_driver build/table_tune
+all: host coll b200 py cli build/parity_driver build/table_tune build/tune_speed
 
 host: $(PKG)/liblagom.so
 
@@ -43,6 +43,10 @@ $(PKG)/liblagom.so: $(HOST_OBJS)
 	$(CXX) -shared -o $@ $^
 
 build/parity_driver: tests/cpp/parity_driver.cpp $(PKG)/liblagom.so
+	@mkdir -p build
+	$(CXX) $(HOST_FLAGS) $< -L$(PKG) -llagom -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
+
+build/tune_speed: tests/cpp/tune_speed.cpp $(PKG)/liblagom.so
 	@mkdir -p build
 	$(CXX) $(HOST_FLAGS) $< -L$(PKG) -llagom -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
