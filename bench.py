@@ -96,6 +96,24 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def tune_speed(binary: str):
+    """Runs tests/cpp/tune_speed.cpp (product: build/tune_speed; reference
+    build: oracle/_ref/tune_speed_ref) pinned to one core; None if absent."""
+    if not os.path.exists(binary):
+        return None
+    cmd = [binary, "7"]
+    if subprocess.run(["which", "taskset"], capture_output=True).returncode == 0:
+        cmd = ["taskset", "-c", "0"] + cmd
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, check=True).stdout
+        d = json.loads(out)
+    except Exception as e:  # reported, never fatal
+        return {"failed": str(e)}
+    return {"unit": "us per tune(start=min), simulator ProfileFn, budget 500, best of 7",
+            "cores": 1, "workloads": {k: {"us": v["us"], "calls": v["calls"], "us_per_call": v["us_per_call"]}
+                                      for k, v in d.items()}}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -364,6 +382,12 @@ def main():
             cpu = json.loads(out.stdout.strip().splitlines()[-1])["cpu_baseline"]
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "port", "sample": f"failed: {e}"}
+        # Search speed (the north star's N = 1 figure of merit): tune(start=min)
+        # with the simulator ProfileFn on the reference's sample workloads,
+        # one pinned host core, best of 7 — the reference build's tuner
+        # (oracle/_ref, the CPU baseline) next to the product's.
+        cpu["reference_tuner"] = tune_speed(os.path.join(ROOT, "oracle", "_ref", "tune_speed_ref"))
+    search_speed = tune_speed(os.path.join(ROOT, "build", "tune_speed")) if world == 1 else None
 
     line = {
         "metric": "overlapped iteration ms (Lagom-tuned collectives + compute)",
@@ -394,6 +418,7 @@ def main():
                     "tflops_isolated": gemm_flops / (y_iso * 1e-3) / 1e12,
                     "frac_of_sustained_bf16": gemm_flops / (y_iso * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"]},
         "roofline": roof,
+        "search_speed": search_speed,
         "e2e": {"value": ms_e2e, "unit": "ms", "h2d_bytes_per_step": T_in_bytes, "d2h_bytes_per_step": 4096},
         "gpu_launches": args.steps * len(dag["comm_ops"]),
         "clocks": result["clocks"],
