@@ -352,8 +352,9 @@ def main():
         achieved = S * fac / (x_dom_iso * 1e-6) / 1e9
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                 "frac": achieved / NVLINK_PEER_GBS, "traffic": None,
+                "frac_of_nominal_900": achieved / 900.0,
                 "note": "busbw of the dominant collective timed alone (comm-only replay, CUDA events); "
-                        "peak = measured NVLink peer copy per direction"}
+                        "peak = measured NVLink peer copy per direction (900 GB/s nominal)"}
     else:
         # n = 1: the collective is a local copy, HBM-bound (read + write)
         achieved = 2 * S / (x_dom_iso * 1e-6) / 1e9
