@@ -56,6 +56,11 @@ class ClockSampler:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
+        # nvidia-smi numbers physical GPUs: map the CUDA ordinal through
+        # CUDA_VISIBLE_DEVICES when it is set
+        vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+        if vis and device < len(vis) and vis[device].strip().isdigit():
+            device = int(vis[device])
         self.device, self.rows, self.proc = device, [], None
 
     def __enter__(self):
