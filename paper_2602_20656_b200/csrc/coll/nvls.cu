@@ -92,7 +92,8 @@ struct NvlsParams {
   unsigned int* abort_flag;
   uint64_t timeout_ns;
   unsigned long long* span;
-  char* peer_recv[LAGOM_MAX_RANKS];  // A2A: recv in every rank's region (peer mappings)
+  char* peer_recv[LAGOM_MAX_RANKS];        // one-hop A2A / AG: recv in every rank's region
+  const char* peer_send[LAGOM_MAX_RANKS];  // one-hop RS: send in every rank's region
 };
 
 __device__ bool nv_wait(const uint64_t* p, uint64_t v, const NvlsParams& P) {
@@ -231,6 +232,37 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
     for (; u0 < hi; u0 += nt) {
       const uint4 v = *reinterpret_cast<const uint4*>(in + u0 * 16);
       for (int k = 1; k <= n; ++k) *reinterpret_cast<uint4*>(P.peer_recv[(r + k) % n] + at + u0 * 16) = v;
+    }
+  } else if constexpr (KIND == 5) {
+    // One-hop ReduceScatter: pull block r of every rank's send through the
+    // peer mappings and combine in the ring order (x_{r+1}, then x_{r+2}, ...,
+    // ending with the own x_r; every combine rounds to the element type), so
+    // the result is bit-identical to the ring schedule and its oracle. No
+    // switch echo: a rank's ingress is its (n-1) peers' blocks only.
+    using R = lagom_dev::Red<T, LAGOM_SUM>;
+    const int64_t at = static_cast<int64_t>(r) * units * 16;
+    int64_t u0 = lo + threadIdx.x;
+    for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+      uint4 acc[U];
+      const char* s1 = P.peer_send[(r + 1) % n] + at;
+#pragma unroll
+      for (int j = 0; j < U; ++j) acc[j] = *reinterpret_cast<const uint4*>(s1 + (u0 + j * nt) * 16);
+      for (int k = 2; k <= n; ++k) {
+        const char* sp = P.peer_send[(r + k) % n] + at;
+        uint4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) v[j] = *reinterpret_cast<const uint4*>(sp + (u0 + j * nt) * 16);
+#pragma unroll
+        for (int j = 0; j < U; ++j) acc[j] = lagom_dev::red4<R>(v[j], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) *reinterpret_cast<uint4*>(P.recv_uc + (u0 + j * nt) * 16) = acc[j];
+    }
+    for (; u0 < hi; u0 += nt) {
+      uint4 acc = *reinterpret_cast<const uint4*>(P.peer_send[(r + 1) % n] + at + u0 * 16);
+      for (int k = 2; k <= n; ++k)
+        acc = lagom_dev::red4<R>(*reinterpret_cast<const uint4*>(P.peer_send[(r + k) % n] + at + u0 * 16), acc);
+      *reinterpret_cast<uint4*>(P.recv_uc + u0 * 16) = acc;
     }
   } else {
   if (KIND == 0) {  // AR: my 1/n share of the channel slice
@@ -378,6 +410,8 @@ const void* pick_nvls(int dtype, int nt) {
     case 8: return pick_nvls_u<KIND, 8, 640>(dtype);
     case 16: return pick_nvls_u<KIND, 16, 640>(dtype);
   }
+  if (KIND == 5)  // one-hop RS holds acc[U] + v[U]: half the unroll of ld_reduce
+    return nt <= 256 ? pick_nvls_u<KIND, 16, 256>(dtype) : pick_nvls_u<KIND, 8, 640>(dtype);
   if (nt <= 256) return pick_nvls_u<KIND, 32, 256>(dtype);
   return (KIND == 1 || KIND == 3 || KIND == 4) ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
 }
@@ -393,19 +427,19 @@ int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 :
 
 // Used by lagom_coll_launch: 1 if this launch can run on the switch, with
 // *kernel/params filled in; 0 to fall back to the P2P kernels.
-// TREE AllGather through peer stores instead of multicast. At n = 2 the
-// multicast echo of the sender's own copy caps NVLS AllGather at ~330 GB/s
-// busbw from NC = 8 upward, while peer stores keep scaling with the channels
-// (4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355 vs 278; NC 32: 569 vs
-// 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl). LAGOM_AG_ONE_HOP=2 follows
-// the config (peer stores at n = 2 and NC >= 12, multicast otherwise; every
-// rank launches the same config, so every rank makes the same choice), 1
-// forces peer stores, 0 / unset keeps multicast. It is off by default: in the
-// FSDP replay at n = 2 the faster AllGather let the search push the
-// ReduceScatter to NC 45-57 and the iteration got slower.
-bool ag_one_hop(int n, int nc) {
+// TREE AllGather / ReduceScatter through the peer mappings (peer stores /
+// peer loads) instead of the switch. At n = 2 the multicast echo of the own
+// block caps NVLS AllGather and ReduceScatter at ~330 GB/s busbw from NC = 8
+// upward, while the one-hop schedules keep scaling with the channels
+// (AllGather on a 4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355 vs 278;
+// NC 32: 569 vs 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl).
+// LAGOM_ONE_HOP=2 follows the config (one hop at n = 2 and NC >= 12, the
+// switch otherwise; every rank launches the same config, so every rank makes
+// the same choice), 1 forces one hop, 0 / unset keeps the switch — the
+// default, see DESIGN.md §6 for the FSDP replay at n = 2.
+bool one_hop(int n, int nc) {
   static const int mode = [] {
-    const char* e = std::getenv("LAGOM_AG_ONE_HOP");
+    const char* e = std::getenv("LAGOM_ONE_HOP");
     return e && *e ? std::atoi(e) : 0;
   }();
   return mode == 1 || (mode == 2 && n == 2 && nc >= 12);
@@ -432,10 +466,15 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
     case LAGOM_ALL_GATHER:
       in_b = a->count * e;
       out_b = a->count * e * n;
-      k = (c->nvls_peers_ready && ag_one_hop(c->nranks, a->num_channels)) ? pick_nvls<4>(a->dtype, a->num_threads)
+      k = (c->nvls_peers_ready && one_hop(c->nranks, a->num_channels)) ? pick_nvls<4>(a->dtype, a->num_threads)
                                                          : pick_nvls<1>(a->dtype, a->num_threads);
       break;
-    case LAGOM_REDUCE_SCATTER: in_b = a->count * e * n; out_b = a->count * e; k = pick_nvls<2>(a->dtype, a->num_threads); break;
+    case LAGOM_REDUCE_SCATTER:
+      in_b = a->count * e * n;
+      out_b = a->count * e;
+      k = (c->nvls_peers_ready && one_hop(c->nranks, a->num_channels)) ? pick_nvls<5>(a->dtype, a->num_threads)
+                                                                      : pick_nvls<2>(a->dtype, a->num_threads);
+      break;
     case LAGOM_ALL_TO_ALL:
       if (!c->nvls_peers_ready) return 0;
       in_b = out_b = a->count * e * n;
@@ -456,7 +495,7 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   if ((a->count * e) % 16 != 0) return 0;  // whole 16 B units per block
   // peer-store kernels (one-hop AllToAll / AllGather) write into peer_recv
   const bool a2a = a->collective == LAGOM_ALL_TO_ALL ||
-                   (a->collective == LAGOM_ALL_GATHER && c->nvls_peers_ready && ag_one_hop(c->nranks, a->num_channels));
+                   (a->collective == LAGOM_ALL_GATHER && c->nvls_peers_ready && one_hop(c->nranks, a->num_channels));
   const bool send_mc = a->collective != LAGOM_ALL_GATHER && !a2a, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
   if ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15) return 0;
   if (send_mc && !inside(c, send, in_b)) return 0;
@@ -473,6 +512,9 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   p.recv_mc = recv_mc && !a2a ? c->nvls_mc + (static_cast<char*>(recv) - c->nvls_uc) : nullptr;
   if (a2a)
     for (int q = 0; q < c->nranks; ++q) p.peer_recv[q] = c->nvls_peer[q] + (static_cast<char*>(recv) - c->nvls_uc);
+  if (a->collective == LAGOM_REDUCE_SCATTER && c->nvls_peers_ready && one_hop(c->nranks, a->num_channels))
+    for (int q = 0; q < c->nranks; ++q)
+      p.peer_send[q] = c->nvls_peer[q] + (static_cast<const char*>(send) - c->nvls_uc);
   p.off_nvbar = c->off_nvbar;
   p.off_nvep = c->off_nvep;
   p.abort_flag = c->abort_dev;

@@ -43,12 +43,13 @@ def test_real_multigpu_parity(world, nvls):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_real_multigpu_parity_one_hop_allgather(world):
-    """TREE AllGather through peer stores (LAGOM_AG_ONE_HOP=1) instead of
-    multicast: bit-exact like every movement collective."""
+def test_real_multigpu_parity_one_hop_allgather_reducescatter(world):
+    """TREE AllGather (peer stores) and ReduceScatter (peer loads, ring order;
+    LAGOM_ONE_HOP=1) instead of
+    the switch: bit-exact (the ReduceScatter combines in the ring order)."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_AG_ONE_HOP="1")
+    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_ONE_HOP="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]
