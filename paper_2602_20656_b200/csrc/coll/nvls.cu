@@ -208,8 +208,15 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
 #pragma unroll
         for (int j = 0; j < U; ++j) *reinterpret_cast<uint4*>(dst + j * nt * 16) = v[j];
       }
-      for (; u0 < hi; u0 += nt)
-        *reinterpret_cast<uint4*>(out + u0 * 16) = *reinterpret_cast<const uint4*>(in + u0 * 16);
+      if (u0 < hi) {  // the rest as one predicated batch
+        uint4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u0 + j * nt < hi) v[j] = *reinterpret_cast<const uint4*>(in + (u0 + j * nt) * 16);
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u0 + j * nt < hi) *reinterpret_cast<uint4*>(out + (u0 + j * nt) * 16) = v[j];
+      }
     }
   } else if constexpr (KIND == 4) {
     // One-hop AllGather (n = 2 default): load the own block once, store it
@@ -229,9 +236,17 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
         for (int j = 0; j < U; ++j) *reinterpret_cast<uint4*>(out + (u0 + j * nt) * 16) = v[j];
       }
     }
-    for (; u0 < hi; u0 += nt) {
-      const uint4 v = *reinterpret_cast<const uint4*>(in + u0 * 16);
-      for (int k = 1; k <= n; ++k) *reinterpret_cast<uint4*>(P.peer_recv[(r + k) % n] + at + u0 * 16) = v;
+    if (u0 < hi) {  // the rest as one predicated batch
+      uint4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (u0 + j * nt < hi) v[j] = *reinterpret_cast<const uint4*>(in + (u0 + j * nt) * 16);
+      for (int k = 1; k <= n; ++k) {
+        char* out = P.peer_recv[(r + k) % n] + at;
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u0 + j * nt < hi) *reinterpret_cast<uint4*>(out + (u0 + j * nt) * 16) = v[j];
+      }
     }
   } else if constexpr (KIND == 5) {
     // One-hop ReduceScatter: pull block r of every rank's send through the
@@ -258,11 +273,25 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
 #pragma unroll
       for (int j = 0; j < U; ++j) *reinterpret_cast<uint4*>(P.recv_uc + (u0 + j * nt) * 16) = acc[j];
     }
-    for (; u0 < hi; u0 += nt) {
-      uint4 acc = *reinterpret_cast<const uint4*>(P.peer_send[(r + 1) % n] + at + u0 * 16);
-      for (int k = 2; k <= n; ++k)
-        acc = lagom_dev::red4<R>(*reinterpret_cast<const uint4*>(P.peer_send[(r + k) % n] + at + u0 * 16), acc);
-      *reinterpret_cast<uint4*>(P.recv_uc + u0 * 16) = acc;
+    if (u0 < hi) {  // the rest as one predicated batch (one round trip per peer)
+      uint4 acc[U];
+      const char* s1 = P.peer_send[(r + 1) % n] + at;
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (u0 + j * nt < hi) acc[j] = *reinterpret_cast<const uint4*>(s1 + (u0 + j * nt) * 16);
+      for (int k = 2; k <= n; ++k) {
+        const char* sp = P.peer_send[(r + k) % n] + at;
+        uint4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u0 + j * nt < hi) v[j] = *reinterpret_cast<const uint4*>(sp + (u0 + j * nt) * 16);
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u0 + j * nt < hi) acc[j] = lagom_dev::red4<R>(v[j], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (u0 + j * nt < hi) *reinterpret_cast<uint4*>(P.recv_uc + (u0 + j * nt) * 16) = acc[j];
     }
   } else {
   if (KIND == 0) {  // AR: my 1/n share of the channel slice
@@ -295,7 +324,18 @@ __global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ Nvls
 #pragma unroll
     for (int k = 0; k < U; ++k) store(dst + k * nt * 16, v[k]);
   }
-  for (; u0 < hi; u0 += nt) store(out + u0 * 16, load(in + u0 * 16));
+  // The rest (< U units per thread) as one predicated batch: its loads are
+  // all in flight together, so it costs one round trip through the switch
+  // instead of one per unit.
+  if (u0 < hi) {
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (u0 + k * nt < hi) v[k] = load(in + (u0 + k * nt) * 16);
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (u0 + k * nt < hi) store(out + (u0 + k * nt) * 16, v[k]);
+  }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
