@@ -101,20 +101,11 @@ def predict(co, link, nc, nt, c, m):
         m / min(nc * co["per_channel_bw"] * eta, link)
 
 
-def fit_all(meas, meas_coll, over, y0, lam):
-    """Fits the reference cost model's coefficients from the measurements
-    (median-relative-error least squares, tools/predict_vs_measured.fit)."""
-    from tools.predict_vs_measured import fit as fit_model
-    params, report = {}, {}
-    for key, pts in meas.items():
-        co, link, rep = fit_model(pts)
-        co.update({"mem_coeff": 0.5, "chunk_knee": 128 * KIB})
-        params[key] = co
-        report[key] = dict(rep, link_bw=link)
-    # victim: SM loss lambda/(lambda-NC) explains part of the slowdown; the
-    # remainder is attributed to the comm's HBM footprint V (wave_time's
-    # blocks*D/(B - V) term) -> kappa, C_knee for RING/SIMPLE.
-    peak = 6434.2e3  # bytes/us, measured copy bandwidth (MEASURED_PEAKS.json)
+def fit_footprint(over, y0, lam, b_chan, peak):
+    """SM loss lambda/(lambda-NC) explains part of the victim's slowdown; the
+    remainder is attributed to the comm's HBM footprint V (wave_time's
+    blocks*D/(B - V) term) -> kappa, C_knee of the subspace (reference
+    mem_footprint, commperf.cpp:127-135)."""
     rows = []
     for nc, c, y, _ in over:
         sm_part = y0 * lam / (lam - nc)
@@ -129,9 +120,25 @@ def fit_all(meas, meas_coll, over, y0, lam):
             best = (err, knee, float(k[0]))
     _, knee, slope = best
     # slope ~ V/(B - V) per (NC*sat) ~= kappa*b_chan/B for V << B
-    b_chan = params["RING/SIMPLE/P2P"]["per_channel_bw"]
-    params["RING/SIMPLE/P2P"]["mem_coeff"] = max(0.0, slope * peak / b_chan)
-    params["RING/SIMPLE/P2P"]["chunk_knee"] = int(knee)
+    return max(0.0, slope * peak / b_chan), int(knee)
+
+
+def fit_all(meas, meas_coll, over, y0, lam, over_tree=()):
+    """Fits the reference cost model's coefficients from the measurements
+    (median-relative-error least squares, tools/predict_vs_measured.fit)."""
+    from tools.predict_vs_measured import fit as fit_model
+    params, report = {}, {}
+    for key, pts in meas.items():
+        co, link, rep = fit_model(pts)
+        co.update({"mem_coeff": 0.5, "chunk_knee": 128 * KIB})
+        params[key] = co
+        report[key] = dict(rep, link_bw=link)
+    peak = 6434.2e3  # bytes/us, measured copy bandwidth (MEASURED_PEAKS.json)
+    for key, ov in (("RING/SIMPLE/P2P", over), ("TREE/SIMPLE/P2P", over_tree)):
+        if ov and key in params:
+            kappa, knee = fit_footprint(ov, y0, lam, params[key]["per_channel_bw"], peak)
+            params[key]["mem_coeff"] = kappa
+            params[key]["chunk_knee"] = knee
     # Per-collective traffic factors, fitted on the TREE key (the subspace
     # the search selects on an NVSwitch box).
     factors, factor_report = {"ALL_REDUCE": 2.0}, {}
@@ -164,7 +171,7 @@ def refit(path, out):
     meas = {k: [tuple(p) for p in v] for k, v in prof["measurements"].items()}
     params, gpu, report, factor_report = fit_all(meas, prof.get("measurements_other", {}),
                                                  prof["victim"]["overlapped"], prof["victim"]["y_alone_us"],
-                                                 prof["gpu"]["num_sms"])
+                                                 prof["gpu"]["num_sms"], prof["victim"].get("overlapped_tree", ()))
     validate(L, gpu, params)
     prof.update(params=params, gpu=gpu, fit_report=report, factor_report=factor_report)
     with open(out, "w") as f:
@@ -242,19 +249,23 @@ def main():
     # victim alone and overlapped (AllReduce ops only)
     eng = engine(dag_ar, "b")
     y0 = json.loads(eng.run_compute_only())["Y"]
-    over = []
+    over, over_tree = [], []
     for nc, c in itertools.product([1, 2, 4, 8, 16, 32], [64 * KIB, 1 * MIB, 4 * MIB]):
         r = json.loads(eng.run(json.dumps({"configs": [cfg("RING", "SIMPLE", nc, 512, c)] * len(sizes)})))
         over.append((nc, c, r["Y"], r["X"]))
+    if ("TREE", "SIMPLE") in keys:  # the in-switch (NVLS) kernels' footprint on the victim
+        for nc, c in itertools.product([1, 2, 4, 8, 16, 32], [64 * KIB, 1 * MIB, 4 * MIB]):
+            r = json.loads(eng.run(json.dumps({"configs": [cfg("TREE", "SIMPLE", nc, 512, c)] * len(sizes)})))
+            over_tree.append((nc, c, r["Y"], r["X"]))
     eng.stop()
     eng.close()
 
     lam = torch.cuda.get_device_properties(local).multi_processor_count
-    params, gpu, report, factor_report = fit_all(meas, meas_coll, over, y0, lam)
+    params, gpu, report, factor_report = fit_all(meas, meas_coll, over, y0, lam, over_tree)
     from paper_2602_20656_b200 import _lagom_py as L2
     validate(L2, gpu, params)
     out = {"nranks": world, "params": params, "gpu": gpu, "fit_report": report, "factor_report": factor_report,
-           "victim": {"y_alone_us": y0, "overlapped": over}, "measurements": meas,
+           "victim": {"y_alone_us": y0, "overlapped": over, "overlapped_tree": over_tree}, "measurements": meas,
            "measurements_other": meas_coll}
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:

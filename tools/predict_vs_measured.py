@@ -70,9 +70,11 @@ def main():
         report[key] = dict(rep, link_bw=lk)
         if key == "RING/SIMPLE/P2P":
             link = lk
-    # footprint from the overlapped-victim sweep (reference mem_footprint form)
-    params["RING/SIMPLE/P2P"]["mem_coeff"] = prof["params"]["RING/SIMPLE/P2P"]["mem_coeff"]
-    params["RING/SIMPLE/P2P"]["chunk_knee"] = prof["params"]["RING/SIMPLE/P2P"]["chunk_knee"]
+    # footprint from the overlapped-victim sweeps (reference mem_footprint form)
+    for key in ("RING/SIMPLE/P2P", "TREE/SIMPLE/P2P"):
+        if key in params and key in prof["params"]:
+            params[key]["mem_coeff"] = prof["params"][key]["mem_coeff"]
+            params[key]["chunk_knee"] = prof["params"][key]["chunk_knee"]
     params["collective_factors"] = prof["params"].get(
         "collective_factors", {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0})
 
@@ -82,6 +84,11 @@ def main():
     dag = dags.BUILDERS[line["config"]["workload"].rsplit("-", 1)[0] if False else _builder(line)](nranks)
     groups = _groups(dag)
     cfgs = [bench["tune"]["configs"][g] for g in groups]
+    # The reference model has ONE link cap (GpuSpec.link_bw, commperf.cpp:112-125):
+    # take the fitted cap of the subspace the tuned configs run in.
+    keys = {f"{c['algorithm']}/{c['protocol']}/{c['transport']}" for c in cfgs}
+    if len(keys) == 1 and next(iter(keys)) in report:
+        link = report[next(iter(keys))]["link_bw"]
     y_iso = np.median([r["y"] for r in raw["compute"]], axis=0)
     lam = prof["gpu"]["num_sms"]
     W = a.waves
