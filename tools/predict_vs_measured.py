@@ -58,6 +58,10 @@ def main():
     ap.add_argument("--bench", required=True)
     ap.add_argument("--out", default="")
     ap.add_argument("--waves", type=int, default=16)
+    ap.add_argument("--hbm-share", type=float, default=0.0,
+                    help="fraction of each isolated wave time put in the wave model's HBM term "
+                         "blocks*D/(B - V) (reference contention.cpp:35-44), the rest in theta; "
+                         "0 = no HBM term (the comm footprint V then has no effect)")
     a = ap.parse_args()
     from paper_2602_20656_b200 import _lagom_py as L
     from paper_2602_20656_b200 import dags
@@ -100,8 +104,8 @@ def main():
     delta = max(0.0, x_over / x_alone - 1.0)
     gpu = dict(prof["gpu"], link_bw=link, compute_on_comm_slowdown=delta)
     work = {"units": {"time": "us", "size": "bytes", "bandwidth": "bytes_per_us"}, "gpu": gpu,
-            "compute_ops": [{"id": c["id"], "total_blocks": lam * W, "blocks_per_sm": 1, "bytes_per_block": 0,
-                             "base_wave_time": float(y) / W} for c, y in zip(dag["compute_ops"], y_iso)],
+            "compute_ops": [compute_op(c["id"], float(y), lam, W, gpu["peak_mem_bw"], a.hbm_share)
+                            for c, y in zip(dag["compute_ops"], y_iso)],
             "comm_ops": []}
     for c in dag["comm_ops"]:
         e = 2 if c.get("dtype", 1) in (1, 2) else 4
@@ -124,6 +128,16 @@ def main():
             json.dump(out, f, indent=1)
         with open(a.out.replace(".json", "_params.json"), "w") as f:
             json.dump(params, f, indent=2)
+
+
+def compute_op(op_id, y_iso, lam, waves, peak, hbm_share):
+    """A compute op calibrated to its isolated time: `waves` full waves of
+    lambda CTAs; a share of each wave's time goes to the HBM term so the
+    comm's footprint V can slow it (f = theta + blocks*D/(B - V))."""
+    f = y_iso / waves
+    d = hbm_share * f * peak / lam  # blocks * D / B = hbm_share * f at V = 0
+    return {"id": op_id, "total_blocks": lam * waves, "blocks_per_sm": 1,
+            "bytes_per_block": int(round(d)), "base_wave_time": f - lam * int(round(d)) / peak}
 
 
 def _builder(line):
