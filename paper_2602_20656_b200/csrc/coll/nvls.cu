@@ -724,11 +724,18 @@ int lagom_comm_nvls_import_peers(lagom_comm_t c, const void* blobs) {
     close(fd);
     if (r != CUDA_SUCCESS) return drv_fail(r, "cuMemImportFromShareableHandle (peer)");
     CUdeviceptr va = 0;
-    CUresult m = DRV(cuMemAddressReserve)(&va, static_cast<size_t>(b.size), g, 0, 0);
-    if (m == CUDA_SUCCESS) m = DRV(cuMemMap)(va, static_cast<size_t>(b.size), 0, h, 0);
+    const size_t size = static_cast<size_t>(b.size);
+    CUresult m = DRV(cuMemAddressReserve)(&va, size, g, 0, 0);
+    const bool reserved = m == CUDA_SUCCESS;
+    bool mapped = false;
+    if (m == CUDA_SUCCESS) mapped = (m = DRV(cuMemMap)(va, size, 0, h, 0)) == CUDA_SUCCESS;
     DRV(cuMemRelease)(h);  // the mapping holds its own reference
-    if (m == CUDA_SUCCESS) m = DRV(cuMemSetAccess)(va, static_cast<size_t>(b.size), &acc, 1);
-    if (m != CUDA_SUCCESS) return drv_fail(m, "map peer NVLS region");
+    if (m == CUDA_SUCCESS) m = DRV(cuMemSetAccess)(va, size, &acc, 1);
+    if (m != CUDA_SUCCESS) {  // undo this peer's partial mapping; earlier peers stay for release
+      if (mapped) DRV(cuMemUnmap)(va, size);
+      if (reserved) DRV(cuMemAddressFree)(va, size);
+      return drv_fail(m, "map peer NVLS region");
+    }
     c->nvls_peer[q] = reinterpret_cast<char*>(va);
   }
   c->nvls_peers_mapped = true;
