@@ -127,19 +127,30 @@ def dist_env():
 
 
 # ----------------------------------------------------------------- reference
+def workload_config(dag: dict) -> dict:
+    """The workload identity shared by both arms' `config` (no engine knobs)."""
+    return {"workload": dag["name"], "compute_ops": len(dag["compute_ops"]), "comm_ops": len(dag["comm_ops"]),
+            "parallelism": dag.get("parallelism", "")}
+
+
+METRIC = "overlapped iteration ms (collectives + compute, one training-step DAG)"
+
+
 def reference_arm(args, world):
-    """The reference's CPU path on the host cores: the CPU collective
-    restatement (oracle/coll_oracle.c; the reference has no data-path
-    collective — a collective there is only comm_time, commperf.cpp:112-125)
-    executing the iteration's collectives over `n` rank buffers in host
-    memory, OpenMP over all host threads. Bounded sample: one layer's comm
-    ops (or at least one op), extrapolated linearly to the whole iteration."""
+    """The reference's CPU path on the host cores. The reference has no
+    data-path collective (a collective there is only comm_time,
+    commperf.cpp:112-125) and no compute path, so its CPU counterpart of the
+    iteration is the CPU collective restatement (oracle/coll_oracle.c,
+    OpenMP over all host threads) executing EVERY comm op of the iteration
+    in order over n rank buffers in host memory. Buffers are allocated and
+    first-touched before the timed region (ops of the same shape share
+    them); each timed step runs all ops back to back."""
+    import collections
     import ctypes
 
     import numpy as np
 
     from paper_2602_20656_b200 import dags
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
     lib_path = os.path.join(ROOT, "oracle", "_ref", "libcoll_oracle.so")
     if not os.path.exists(lib_path):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "coll"], check=True, capture_output=True)
@@ -152,45 +163,104 @@ def reference_arm(args, world):
     dag = dags.BUILDERS[args.workload](n)
     ops = dag["comm_ops"]
     coll_codes = {"ALL_REDUCE": 0, "ALL_GATHER": 1, "REDUCE_SCATTER": 2, "ALL_TO_ALL": 3}
-    layer_ops = [c for c in ops if c.get("ready_after") in (None, dag["compute_ops"][0]["id"])] or ops[:1]
     rng = np.random.default_rng(0)
-
-    def run_op(c):
+    # Prefaulted host buffers: per (collective, count) a pool of buffer sets
+    # that ops of that shape rotate through, sized so consecutive ops never
+    # find their data in the last-level cache (>= 1.5 GiB per pool, or one
+    # set per op).
+    bufs, uses = {}, collections.Counter((c["collective"], c["count"]) for c in ops)
+    for c in ops:
+        key = (c["collective"], c["count"])
+        if key in bufs:
+            continue
         code = coll_codes[c["collective"]]
-        cnt = c["count"]
-        nin = cnt if code in (0, 1) else cnt * n
-        nout = cnt if code in (0, 2) else cnt * n
-        sends = [rng.integers(0, 1 << 16, size=nin, dtype=np.uint16) for _ in range(n)]
-        outs = [np.empty(nout, dtype=np.uint16) for _ in range(n)]
-        s = (ctypes.c_void_p * n)(*[a.ctypes.data for a in sends])
-        r = (ctypes.c_void_p * n)(*[a.ctypes.data for a in outs])
-        t0 = time.perf_counter()
-        rc = lib.lagom_oracle_collective(code, 0, n, 1, 0, cnt, s, r)
-        dt = time.perf_counter() - t0
-        assert rc == 0
-        return dt
+        nin = c["count"] * (n if code in (2, 3) else 1)
+        nout = c["count"] * (n if code in (1, 3) else 1)
+        set_bytes = 2 * n * (nin + nout)
+        pool = []
+        for _ in range(max(1, min(uses[key], -(-(3 << 29) // set_bytes)))):
+            sends = [rng.integers(0x3000, 0x3f80, size=nin, dtype=np.uint16) for _ in range(n)]  # finite bf16
+            outs = [np.ones(nout, dtype=np.uint16) for _ in range(n)]  # written: pages faulted in
+            pool.append((sends, outs, (ctypes.c_void_p * n)(*[a.ctypes.data for a in sends]),
+                         (ctypes.c_void_p * n)(*[a.ctypes.data for a in outs])))
+        bufs[key] = (code, pool)
+    turn = collections.Counter()
 
-    scale = len(ops) / len(layer_ops)
-    for _ in range(min(1, args.warmup)):
-        run_op(layer_ops[0])
-    steps = []
-    for _ in range(args.steps):
-        steps.append(sum(run_op(c) for c in layer_ops) * scale)
+    def step():
+        t0 = time.perf_counter()
+        for c in ops:
+            key = (c["collective"], c["count"])
+            code, pool = bufs[key]
+            _, _, s, r = pool[turn[key] % len(pool)]
+            turn[key] += 1
+            # ring order (algorithm 0) and bf16 (dtype 1), sum
+            if lib.lagom_oracle_collective(code, 0, n, 1, 0, c["count"], s, r) != 0:
+                raise RuntimeError("oracle collective failed")
+        return time.perf_counter() - t0
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    steps = [step() for _ in range(args.steps)]
     ms = statistics.median(steps) * 1e3
     cores = lib.lagom_oracle_threads()
-    sample = (f"{len(layer_ops)} of {len(ops)} comm ops (one layer) per step, x{scale:.0f} to the "
-              f"iteration; n={n} rank buffers in host memory; no GEMMs (the reference path has none)")
-    line = {"metric": "overlapped iteration ms (Lagom-tuned collectives + compute)", "impl": "reference",
-            "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+    sample = (f"all {len(ops)} comm ops of one iteration per step (the whole workload), bf16 sum, ring order, "
+              f"n={n} rank buffers in host memory (prefaulted, rotated so no op finds its data in cache), OpenMP "
+              f"over {cores} threads; the iteration's GEMMs are not executed (the reference has no compute path)")
+    line = {"metric": METRIC, "impl": "reference",
+            "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": max(1, args.warmup),
             "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": dag["name"], "comm_ops": len(ops), "parallelism": f"dp{world}"},
+            "dtype": "bf16", "data": "synthetic", "config": workload_config(dag),
             "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------- lagom
+def nccl_log_env(tag: str) -> str | None:
+    """NCCL_DEBUG=INFO with INIT/TUNING to a per-process file, unless the
+    user set NCCL_DEBUG: the channels and algorithms NCCL chose for the
+    baseline go into the bench line."""
+    if os.environ.get("NCCL_DEBUG"):
+        return None
+    path = f"/tmp/lagom_nccl_{tag}_%p.log"
+    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,TUNING", NCCL_DEBUG_FILE=path)
+    return path.replace("%p", str(os.getpid()))
+
+
+def nccl_log_summary(path: str | None) -> dict:
+    import re
+    if not path or not os.path.exists(path):
+        return {"log": None}
+    text = open(path, errors="replace").read()
+    out = {"log": path}
+    m = re.search(r"(\d+) coll channels, (\d+) collnet channels, (\d+) nvls channels, (\d+) p2p channels", text)
+    if m:
+        out.update(coll_channels=int(m.group(1)), nvls_channels=int(m.group(3)), p2p_channels=int(m.group(4)))
+    algo = [ln.split("NCCL INFO", 1)[-1].strip() for ln in text.splitlines()
+            if re.search(r"(AllReduce|AllGather|ReduceScatter|SendRecv|Broadcast).*(Algo|algorithm|proto)", ln)]
+    out["tuning"] = sorted(set(algo))[:12]
+    out["version"] = (re.search(r"NCCL version ([\w.+]+)", text) or [None, None])[1]
+    return out
+
+
+def wire_bytes(op: dict, n: int, cfg: dict, nvls: bool, one_hop_a2a: bool) -> tuple[float, str]:
+    """Bytes that cross NVLink per rank, per direction, for one launch of the
+    config's schedule, and the schedule's name. n = 1: HBM
+    bytes (read + write of the local copy)."""
+    e = 2 if op["dtype"] in (1, 2) else 4
+    coll = op["collective"]
+    S = op["count"] * e * (1 if coll == "ALL_REDUCE" else n)  # nccl-tests algorithmic bytes
+    if n == 1:
+        return 2.0 * op["count"] * e, "local copy (HBM read + write)"
+    tree = cfg["algorithm"] == "TREE"
+    if tree and nvls and coll in ("ALL_REDUCE", "ALL_GATHER", "REDUCE_SCATTER"):
+        return float(S), "NVLS (in-switch): S per rank on the busier direction"
+    if tree and coll == "ALL_TO_ALL" and one_hop_a2a:
+        return S * (n - 1) / n, "one-hop AllToAll: (n-1)/n S egress"
+    f = 2.0 * (n - 1) / n if coll == "ALL_REDUCE" else (n - 1) / n
+    return S * f, "ring: busbw bytes"
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -207,9 +277,16 @@ def main():
     ap.add_argument("--params", default=os.path.join(ROOT, "profiles", "fitted_params_b200_n4.json"),
                     help="subspace params fitted on B200 by tools/contention_profile.py (reference JSON "
                          "schema); '' = the reference's synthetic defaults")
-    ap.add_argument("--sm-reserve", type=int, default=1,
-                    help="Lagom replays run each compute op's GEMMs on num_sms - max NC of the collectives "
-                         "that can overlap it (cuBLASLt SM count target)")
+    ap.add_argument("--sm-partition", type=int, default=1, choices=[0, 1, 2],
+                    help="GEMMs a collective can overlap run on num_sms - NC SMs: 0 never, 1 only for "
+                         "collectives whose CTAs cannot share an SM with a GEMM CTA (default), 2 always")
+    ap.add_argument("--coresident", type=int, default=1,
+                    help="NVLS / one-hop / single-rank kernels sized to co-reside with GEMM CTAs")
+    ap.add_argument("--one-hop", type=int, default=0, help="lagom_comm_opts_t.one_hop (TREE AG/RS schedule)")
+    ap.add_argument("--ablations", type=int, default=1,
+                    help="also time: our kernels at the seed with the SM partition forced on, and (N > 1) NCCL "
+                         "with the GEMMs on num_sms - NCCL's channels")
+    ap.add_argument("--order-seed", type=int, default=20260219, help="seed of the per-step arm permutation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -220,6 +297,8 @@ def main():
         if rank == 0:
             reference_arm(args, world)
         return
+
+    import random
 
     import torch
     import torch.distributed as dist
@@ -235,6 +314,7 @@ def main():
         token = tok[0]
     else:
         token = secrets.token_hex(6)
+    nccl_log = nccl_log_env(token) if not args.no_nccl else None
     peaks = load_peaks()
     n_sms = torch.cuda.get_device_properties(local).multi_processor_count
     gpu_json = json.dumps({"num_sms": n_sms, "peak_mem_bw": peaks["hbm_gbs"] * 1e3,
@@ -255,8 +335,10 @@ def main():
     T_in_bytes = 8192 * 2048 * 2
     eng = L.ReplayEngine(json.dumps(dag), f"lagom_{token}", rank, world, local, repeats=1, warmup=0,
                          nccl=not args.no_nccl, e2e_in_bytes=T_in_bytes, e2e_out_bytes=4096,
-                         reserve_comm_sms=bool(args.sm_reserve), max_channels=max(32, args.nc_max),
-                         nvls=bool(args.nvls))
+                         sm_partition=args.sm_partition, max_channels=max(32, args.nc_max),
+                         nvls=bool(args.nvls), coresident=bool(args.coresident), one_hop=args.one_hop)
+    nvls_state = {"requested": bool(args.nvls) and world > 1, "active": bool(eng.nvls_active),
+                  "peer_mappings": bool(eng.nvls_peers_active)}
     result, tuned, tune_wall_s, tune_runs = None, None, 0.0, {}
     if rank != 0:
         eng.serve()
@@ -267,6 +349,7 @@ def main():
         t_tune = time.perf_counter()
         eng.run_compute_only()  # first-touch / clocks settle before the search
         starts = ["min", "nccl-default"] if args.start == "best" else [args.start]
+        eng.set_partition(args.sm_partition, 0)
         eng.set_measurement(5, 2)  # each profile call: median of 5 replays after 2 warmups
         params_doc = open(args.params).read() if args.params and os.path.exists(args.params) else ""
         if params_doc:
@@ -296,35 +379,54 @@ def main():
         cfg_doc = json.dumps({"configs": full_cfgs})
         ncc_doc = json.dumps({"configs": seed_full})
 
-        def series(fn, k):
-            return [json.loads(fn()) for _ in range(k)]
+        # ---- 2. measured full-iteration replays. Every step runs every arm
+        # once, in a fresh seeded random order (a power-capped B200 runs a
+        # replay faster right after a lighter one, so no arm may keep a fixed
+        # predecessor); compute-only is one of the arms.
+        nccl_reserve = 0
 
-        # ---- 2. measured full-iteration replays. The arms are interleaved
-        # step by step (lagom, nccl, seed, e2e, ...) so that clock/power drift
-        # of the power-capped part affects every arm alike.
-        arms = {"lagom": lambda: eng.run(cfg_doc), "e2e": lambda: eng.run_e2e(cfg_doc),
-                "seed": lambda: eng.run(ncc_doc)}
+        def with_partition(part, nccl_res, fn):
+            def run():
+                eng.set_partition(part, nccl_res)
+                return fn()
+            return run
+
+        arms = {"lagom": with_partition(args.sm_partition, 0, lambda: eng.run(cfg_doc)),
+                "e2e": with_partition(args.sm_partition, 0, lambda: eng.run_e2e(cfg_doc)),
+                "seed": with_partition(args.sm_partition, 0, lambda: eng.run(ncc_doc)),
+                "compute": eng.run_compute_only}
+        if args.ablations:
+            arms["seed_partition_all"] = with_partition(2, 0, lambda: eng.run(ncc_doc))
         if not args.no_nccl:
-            arms["nccl"] = eng.run_nccl
+            arms["nccl"] = with_partition(args.sm_partition, 0, eng.run_nccl)
+            eng.run_nccl()  # NCCL initialises its channels on the first collective
+            nccl_info = nccl_log_summary(nccl_log)
+            if args.ablations and world > 1:
+                nccl_reserve = int(nccl_info.get("nvls_channels") or nccl_info.get("coll_channels") or 0) \
+                    if nvls_state["active"] else int(nccl_info.get("coll_channels") or 0)
+                if nccl_reserve > 0:
+                    arms["nccl_partition"] = with_partition(args.sm_partition, nccl_reserve, eng.run_nccl)
+        else:
+            nccl_info = {}
         for _ in range(args.warmup):
             for fn in arms.values():
                 fn()
         runs = {k: [] for k in arms}
-        # The arm order rotates every step: on a power-capped part a replay
-        # runs faster right after a lighter one, so no arm keeps a fixed
-        # predecessor.
         names = list(arms)
+        rng = random.Random(args.order_seed)
+        orders = []
         with ClockSampler(local) as clk:
             for s in range(args.steps):
-                for k in names[s % len(names):] + names[:s % len(names)]:
+                perm = names[:]
+                rng.shuffle(perm)
+                orders.append(perm)
+                for k in perm:
                     runs[k].append(json.loads(arms[k]()))
-        lagom_runs, e2e_runs, seed_runs = runs["lagom"], runs["e2e"], runs["seed"]
-        nccl_runs = runs.get("nccl", [])
-        compute_only = series(eng.run_compute_only, max(3, args.steps // 3))
-        comm_only = series(lambda: eng.run_comm_only(cfg_doc), max(3, args.steps // 3))
+        eng.set_partition(args.sm_partition, 0)
+        comm_only = [json.loads(eng.run_comm_only(cfg_doc)) for _ in range(max(3, args.steps // 3))]
         eng.stop()
-        result = dict(lagom=lagom_runs, e2e=e2e_runs, compute=compute_only, comm=comm_only,
-                      seed=seed_runs, nccl=nccl_runs, clocks=clk.summary())
+        result = dict(runs, comm=comm_only, clocks=clk.summary(), orders=orders, nccl_reserve=nccl_reserve,
+                      nccl_info=nccl_info)
     eng.close()  # collective: NCCL teardown on every rank at the same point
     if world > 1:
         dist.barrier()
@@ -333,15 +435,13 @@ def main():
 
     # ---- 3. report
     med = lambda rs, k="Z": statistics.median(r[k] for r in rs) if rs else None  # noqa: E731
-    ms = med(result["lagom"]) / 1e3
-    ms_e2e = med(result["e2e"]) / 1e3
-    ms_nccl = med(result["nccl"]) / 1e3 if result["nccl"] else None
-    ms_seed = med(result["seed"]) / 1e3
-    y_iso = med(result["compute"], "Y") / 1e3
-    y_lagom = med(result["lagom"], "Y") / 1e3
-    y_nccl = med(result["nccl"], "Y") / 1e3 if result["nccl"] else None
+    ms = {k: med(result[k]) / 1e3 for k in arms}
+    y = {k: med(result[k], "Y") / 1e3 for k in arms}
+    ms_nccl = ms.get("nccl")
+    y_iso = y["compute"]
 
-    # dominant kernel: the comm op with the largest summed x over the DAG
+    # dominant kernel: the comm op with the largest summed x over the DAG,
+    # timed alone at its tuned config (comm-only replay)
     import collections
     x_sum = collections.defaultdict(float)
     for r in result["lagom"]:
@@ -349,34 +449,36 @@ def main():
             x_sum[j] += x
     j_dom = max(x_sum, key=x_sum.get) if x_sum else 0
     op = dag["comm_ops"][j_dom]
-    x_dom_us = statistics.median(r["x"][j_dom] for r in result["lagom"])
-    x_dom_iso = statistics.median(r["x"][j_dom] for r in result["comm"])
-    S = op["count"] * 2 * (1 if op["collective"] == "ALL_REDUCE" else world)
-    fac = {"ALL_REDUCE": 2.0 * (world - 1) / world}.get(op["collective"], (world - 1) / world) if world > 1 else 0
+    cfg_dom = full_cfgs[j_dom]
+    t_ev = statistics.median(r["x_ev"][j_dom] for r in result["comm"])    # CUDA events, us
+    t_span = statistics.median(r["x"][j_dom] for r in result["comm"])     # kernel's own span, us
+    wb, sched = wire_bytes(op, world, cfg_dom, nvls_state["active"], nvls_state["peer_mappings"])
+    e = 2 if op["dtype"] in (1, 2) else 4
+    S = op["count"] * e * (1 if op["collective"] == "ALL_REDUCE" else world)
     if world > 1:
-        achieved = S * fac / (x_dom_iso * 1e-6) / 1e9
+        achieved = wb / (t_ev * 1e-6) / 1e9
+        busf = 2.0 * (world - 1) / world if op["collective"] == "ALL_REDUCE" else (world - 1) / world
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                 "frac": achieved / NVLINK_PEER_GBS, "traffic": None,
-                "frac_of_nominal_900": achieved / 900.0,
-                "note": "busbw of the dominant collective timed alone (comm-only replay, CUDA events); "
-                        "peak = measured NVLink peer copy per direction (900 GB/s nominal)"}
+                "busbw": S * busf / (t_ev * 1e-6) / 1e9,
+                "note": f"{op['collective']} {S / 2**20:.1f} MiB at its tuned config, timed alone with CUDA "
+                        f"events (comm-only replay); achieved = wire bytes per rank on the busier direction "
+                        f"({sched}) / time; peak = measured NVLink peer copy per direction (900 nominal)"}
     else:
-        # n = 1: the collective is a local copy, HBM-bound (read + write)
-        achieved = 2 * S / (x_dom_iso * 1e-6) / 1e9
+        achieved = wb / (t_ev * 1e-6) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "note": f"n=1 collective = local copy; peak = {peaks['_source']} copy bandwidth"}
-    # The Lagom picks run the collective on a few SMs by design; the per-SM
-    # rate against the per-SM share of the peak shows how hard those SMs work.
-    nc_dom = int(tuned["configs"][groups[j_dom]]["num_channels"])
-    roof["channels"] = nc_dom
-    roof["achieved_per_sm"] = roof["achieved"] / max(1, nc_dom)
-    if world == 1:  # HBM is shared by all SMs: compare with one SM's share
-        roof["peak_per_sm_share"] = roof["peak"] / n_sms
+                "note": f"n=1: the collective is a local copy of {S / 2**20:.1f} MiB ({sched}), timed alone with "
+                        f"CUDA events at the tuned config; peak = {peaks['_source']} copy bandwidth"}
+    nc_dom = int(cfg_dom["num_channels"])
+    roof.update(config=f"{cfg_dom['algorithm']}/{cfg_dom['protocol']}/NC{nc_dom}/NT{cfg_dom['num_threads']}",
+                kernel_span_us=t_span, event_us=t_ev, achieved_per_cta=roof["achieved"] / max(1, nc_dom))
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
-            roof["traffic"] = json.load(f).get(f"{dag['name']}", None)
+            tr = json.load(f).get(f"{dag['name']}")
+        if isinstance(tr, dict) and tr.get("config") == roof["config"]:
+            roof["traffic"] = tr.get("bytes")
 
     gemm_flops = dags.flops(dag)
     cpu = None
@@ -395,38 +497,51 @@ def main():
         cpu["reference_tuner"] = tune_speed(os.path.join(ROOT, "oracle", "_ref", "tune_speed_ref"))
     search_speed = tune_speed(os.path.join(ROOT, "build", "tune_speed")) if world == 1 else None
 
+    same_cfg = full_cfgs == seed_full
+    our_arms = [k for k in ("lagom", "e2e", "seed", "seed_partition_all") if k in arms]
+    launches_per_replay = sum(1 for c in dag["comm_ops"] if c["count"] > 0)
     line = {
-        "metric": "overlapped iteration ms (Lagom-tuned collectives + compute)",
-        "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC,
+        "value": ms["lagom"], "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms["lagom"], "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights/activations on device)",
-        "config": {"workload": dag["name"], "compute_ops": len(dag["compute_ops"]),
-                   "comm_ops": len(dag["comm_ops"]), "parallelism": dag.get("parallelism", f"dp{world}"),
-                   "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
-                   "sm_partition": "per compute op: GEMMs on num_sms - max NC of overlappable collectives"
-                   if args.sm_reserve else "none",
-                   "params": os.path.relpath(args.params, ROOT) if args.params else "reference defaults",
-                   "nvls": bool(args.nvls) and world > 1,
-                   "tune": {"start": tuned["start"], "others": tuned["other_starts"],
-                            "groups": len(tuned["configs"]),
-                            "profile_calls": tuned["profile_calls"], "boundary": tuned["boundary_condition"],
-                            "search_wall_s": round(tune_wall_s, 3),
-                            "search_calls_total": sum(r["profile_calls"] for r in tune_runs.values()),
-                            "ms_per_profile_call": round(1e3 * tune_wall_s /
-                                                         max(1, sum(r["profile_calls"] for r in tune_runs.values())), 3),
-                            "picks": [f"{c['algorithm']}/{c['protocol']}/NC{c['num_channels']}/NT"
-                                      f"{c['num_threads']}/C{c['chunk_size'] // 1024}K" for c in tuned["configs"]]}},
-        "nccl_default_ms": ms_nccl,
-        "speedup_vs_nccl_default": (ms_nccl / ms) if ms_nccl else None,
-        "lagom_kernels_nccl_seed_ms": ms_seed,
-        "compute": {"isolated_ms": y_iso, "overlapped_ms": y_lagom, "overlapped_nccl_ms": y_nccl,
-                    "slowdown": y_lagom / y_iso, "slowdown_nccl": (y_nccl / y_iso) if y_nccl else None,
+        "config": workload_config(dag),
+        "speedup_vs_nccl_default": (ms_nccl / ms["lagom"]) if ms_nccl else None,
+        "arms_ms": ms,
+        "ablation": {
+            "nccl_default": ms_nccl,
+            "nccl_with_sm_partition": ms.get("nccl_partition"),
+            "nccl_reserved_sms": result["nccl_reserve"] or None,
+            "ours_at_seed_no_partition" if args.sm_partition != 2 else "ours_at_seed": ms["seed"],
+            "ours_at_seed_partition_all": ms.get("seed_partition_all"),
+            "ours_tuned": ms["lagom"],
+            "tuned_equals_seed": same_cfg,
+            "noise_floor_ms": abs(ms["lagom"] - ms["seed"]) if same_cfg else None,
+            "order": "seeded random permutation of all arms per step (compute-only included)",
+        },
+        "compute": {"isolated_ms": y_iso, "overlapped_ms": y["lagom"], "overlapped_nccl_ms": y.get("nccl"),
+                    "slowdown": y["lagom"] / y_iso, "slowdown_nccl": (y["nccl"] / y_iso) if "nccl" in y else None,
                     "tflops_isolated": gemm_flops / (y_iso * 1e-3) / 1e12,
                     "frac_of_sustained_bf16": gemm_flops / (y_iso * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"]},
         "roofline": roof,
+        "lagom": {"sm_partition": ["none", "auto (non-co-resident kernels only)", "all"][args.sm_partition],
+                  "coresident_kernels": bool(args.coresident), "one_hop": args.one_hop,
+                  "params": os.path.relpath(args.params, ROOT) if args.params else "reference defaults",
+                  "nvls": nvls_state, "nccl": result["nccl_info"],
+                  "l2": "inputs larger than L2 (weights+activations per step >> 126 MB)",
+                  "tune": {"start": tuned["start"], "others": tuned["other_starts"], "groups": len(tuned["configs"]),
+                           "profile_calls": tuned["profile_calls"], "boundary": tuned["boundary_condition"],
+                           "search_wall_s": round(tune_wall_s, 3),
+                           "search_calls_total": sum(r["profile_calls"] for r in tune_runs.values()),
+                           "ms_per_profile_call": round(1e3 * tune_wall_s /
+                                                        max(1, sum(r["profile_calls"] for r in tune_runs.values())), 3),
+                           "picks": [f"{c['algorithm']}/{c['protocol']}/NC{c['num_channels']}/NT"
+                                     f"{c['num_threads']}/C{c['chunk_size'] // 1024}K" for c in tuned["configs"]]}},
         "search_speed": search_speed,
-        "e2e": {"value": ms_e2e, "unit": "ms", "h2d_bytes_per_step": T_in_bytes, "d2h_bytes_per_step": 4096},
-        "gpu_launches": args.steps * len(dag["comm_ops"]),
+        "e2e": {"value": ms["e2e"], "unit": "ms", "h2d_bytes_per_step": T_in_bytes, "d2h_bytes_per_step": 4096},
+        "gpu_launches": args.steps * len(our_arms) * launches_per_replay,
+        "gpu_launches_note": f"our collective kernels in the timed region: {launches_per_replay} per replay x "
+                             f"{len(our_arms)} arms ({', '.join(our_arms)}) x {args.steps} steps",
         "clocks": result["clocks"],
         "cpu_baseline": cpu,
     }
@@ -434,10 +549,10 @@ def main():
     if args.out:
         # measured Chrome traces (reference trace schema) of one Lagom and one NCCL step
         for arm in ("lagom", "nccl"):
-            if result[arm]:
+            if result.get(arm):
                 with open(args.out.replace(".json", f"_trace_{arm}.json"), "w") as f:
                     json.dump(result[arm][len(result[arm]) // 2].get("trace", []), f)
-        for arm in ("lagom", "e2e", "seed", "nccl", "compute", "comm"):
+        for arm in list(arms) + ["comm"]:
             for r in result[arm]:
                 r.pop("trace", None)
         with open(args.out, "w") as f:

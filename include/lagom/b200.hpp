@@ -87,6 +87,12 @@ std::unique_ptr<Coordinator> make_shm_coordinator(const std::string& name, int r
                                                   double timeout_s = 300.0);
 
 // ---------------------------------------------------------------- engine ---
+// Per-SM resources an sm_100 cuBLASLt bf16 GEMM CTA leaves free (256 threads
+// x 168 registers, ~214 KB shared memory; profiles/round2_coresidence.md).
+constexpr int kCoresidentRegs = 21845;      // 65536 / 3
+constexpr int kCoresidentSmem = 16 * 1024;
+enum : int { kPartitionNone = 0, kPartitionAuto = 1, kPartitionAll = 2 };
+
 struct ReplayOptions {
   int device = 0;
   int repeats = 3;           // replays per profile call; medians are reported
@@ -101,13 +107,27 @@ struct ReplayOptions {
   // result back to pinned host memory; both copies are inside Z.
   std::int64_t e2e_in_bytes = 0;
   std::int64_t e2e_out_bytes = 0;
-  // SM partition: in Lagom modes the GEMMs run with cuBLASLt's SM count
-  // target = num_sms - max NC of the configs, so collective CTAs never
-  // queue behind persistent GEMM CTAs (NCCL-baseline replays keep cuBLASLt's
-  // default). This is the contention model's lambda - NC made explicit.
-  bool reserve_comm_sms = false;
+  // SM partition of Lagom replays: the GEMMs that a collective can overlap
+  // run with cuBLASLt's SM count target = num_sms - the NC it reserves
+  // (the contention model's lambda - NC made explicit).
+  //   kPartitionNone: no SMs reserved;
+  //   kPartitionAuto: only collectives whose CTAs cannot share an SM with a
+  //     GEMM CTA reserve their NC (lagom_coll_footprint: NT x registers >
+  //     kCoresidentRegs or shared memory > kCoresidentSmem) — the
+  //     co-resident NVLS / one-hop / single-rank kernels take no SMs;
+  //   kPartitionAll: every collective reserves its NC (round 1).
+  // NCCL-baseline replays keep cuBLASLt's default (see nccl_reserve_sms).
+  int sm_partition = 1;
+  // Ablation: NCCL-baseline replays run the GEMMs that a collective can
+  // overlap on num_sms - nccl_reserve_sms SMs (0: cuBLASLt's default).
+  int nccl_reserve_sms = 0;
   // SIMPLE collectives move data with TMA bulk copies (lagom_comm_opts_t.use_tma).
   bool use_tma = true;
+  // lagom_comm_opts_t.coresident / one_hop / a2a_tma (kernel selection; the
+  // same on every rank).
+  bool coresident = true;
+  int one_hop = 0;
+  bool a2a_tma = false;
   // NVSwitch multicast: comm buffers live in an NVLS region, so TREE
   // AllReduce/AllGather/ReduceScatter run reduced/broadcast in the switch.
   bool nvls = false;
@@ -117,6 +137,10 @@ struct ReplayOptions {
 struct ReplayMeasurement {
   ProfileResult profile;           // x_j, X = sum x_j, Y = sum y_i, Z
   std::vector<double> comp_times;  // y_i
+  // x_j from CUDA events on the comm stream (launch to completion, including
+  // time queued behind other kernels), next to profile.comm_times, which is
+  // the kernel's own active span for the Lagom kernels
+  std::vector<double> comm_event_times;
   double wall_us = 0.0;            // host wall time of the profile call
   // This rank's last replay as a timeline (one event per compute op on the
   // "compute" stream, one per comm op on "comm"), start offsets from the
@@ -162,6 +186,16 @@ class ReplayEngine {
   // Rank 0: replays per measurement and unrecorded warmups for the following
   // remote_* calls (sent along with each command to the serving ranks).
   void set_measurement(int repeats, int warmup);
+  // Rank 0: the SM partition of the following remote_* calls (sent along
+  // with each command): Lagom replays reserve max NC SMs from the GEMMs that
+  // a collective can overlap (lagom_partition), NCCL replays reserve
+  // `nccl_reserve_sms` (0 = none).
+  void set_partition(int sm_partition, int nccl_reserve_sms);
+  // Whether the NVLS region (in-switch TREE) and the peer mappings (one-hop
+  // AllToAll / AllGather / ReduceScatter) are in use — what set-up achieved,
+  // not what was requested.
+  bool nvls_active() const;
+  bool nvls_peers_active() const;
 
  private:
   struct Impl;

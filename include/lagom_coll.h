@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LAGOM_COLL_ABI_VERSION 1
+#define LAGOM_COLL_ABI_VERSION 2
 #define LAGOM_MAX_RANKS 8
 #define LAGOM_MAX_CHANNELS 64
 #define LAGOM_HANDLE_BYTES 64 /* == sizeof(cudaIpcMemHandle_t) */
@@ -63,11 +63,25 @@ typedef struct {
   int64_t timeout_ms;      /* spin-wait watchdog; default 10000                         */
   int use_tma;             /* SIMPLE copy steps use TMA bulk copies (1, default); 2 also
                               routes reduction steps through the TMA smem ring; 0 off  */
+  /* Options below change which kernel a launch runs, so every rank of a
+   * communicator must use the same values: lagom_comm_import_handles checks
+   * them against every peer's and fails with LAGOM_ERR_INVALID_ARGUMENT. */
+  int coresident;          /* 1 (default): the NVLS, one-hop and single-rank kernels
+                              fit next to a GEMM CTA on one SM (<= 21.8 K registers per
+                              CTA, no dynamic shared memory), so NC costs no SMs; 0:
+                              deeper unrolls (more registers) at the same NC/NT      */
+  int one_hop;             /* TREE AllGather / ReduceScatter with NVLS bound: 0 (default)
+                              through the switch, 1 one hop over the peer mappings, 2
+                              one hop at nranks == 2 and NC >= 12                      */
+  int a2a_tma;             /* one-hop AllToAll through the TMA engine (192 KB smem ring
+                              per CTA, cannot share an SM with a GEMM); default 0      */
 } lagom_comm_opts_t;
 
 typedef struct {
   int collective;       /* lagom_collective_t */
-  int algorithm;        /* lagom_algorithm_t (TREE: ALL_REDUCE only) */
+  int algorithm;        /* lagom_algorithm_t (TREE: the binary tree for ALL_REDUCE; with
+                           NVLS bound, in-switch AR/AG/RS and the one-hop AllToAll;
+                           otherwise the other collectives run their ring schedule) */
   int protocol;         /* lagom_protocol_t */
   int num_channels;     /* NC: CTAs */
   int num_threads;      /* NT: threads per CTA */
@@ -124,12 +138,25 @@ int lagom_comm_check(lagom_comm_t comm);
  * without launching. */
 int lagom_coll_validate(lagom_comm_t comm, const lagom_coll_args_t* args);
 
-/* Real mode: enqueue one collective on `stream` (cudaStream_t). */
+/* Real mode: enqueue one collective on `stream` (cudaStream_t). Launches on
+ * one communicator are ordered in issue order even across streams (each
+ * launch waits for the previous one through an event the communicator
+ * keeps), because consecutive launches share the per-connection step
+ * counters and the NVLS epochs. With nranks == 1 every collective is a copy
+ * of count elements (none in place). */
 int lagom_coll_launch(lagom_comm_t comm, const lagom_coll_args_t* args, const void* sendbuf,
                       void* recvbuf, void* stream);
 /* Virtual mode: sendbufs/recvbufs hold nranks device pointers, rank order. */
 int lagom_coll_launch_virtual(lagom_comm_t comm, const lagom_coll_args_t* args,
                               const void* const* sendbufs, void* const* recvbufs, void* stream);
+
+/* The per-CTA footprint of the kernel this launch would run (nothing is
+ * launched): registers per thread and shared memory per CTA (static +
+ * dynamic); both 0 when nothing would launch (count 0, in-place nranks 1).
+ * NT x regs and smem tell whether the CTAs fit next to a GEMM CTA on one SM
+ * (sm_100 cuBLASLt bf16 GEMMs leave ~22.5 K registers and ~19 KB free). */
+int lagom_coll_footprint(lagom_comm_t comm, const lagom_coll_args_t* args, const void* sendbuf,
+                         void* recvbuf, int* regs_per_thread, int* smem_bytes);
 
 /* Algorithmic and bus bytes of one launch (nccl-tests accounting):
  * algbw bytes S and busbw factor, so busbw = S / t * factor. */

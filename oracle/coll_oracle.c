@@ -116,16 +116,6 @@ long long lagom_oracle_ring_block(long long count, int nranks, int dtype) {
   return (per + pack - 1) / pack * pack;
 }
 
-/* Ring reduction of element offset `i` (in each rank's input) for block k. */
-static void ring_reduce(int dtype, int op, int n, int k, const char* const* send, long long byte_off,
-                        char* out) {
-  const int e = esize(dtype);
-  char acc[4];
-  memcpy(acc, send[(k + 1) % n] + byte_off, (size_t)e);
-  for (int h = 2; h <= n; ++h) combine(dtype, op, acc, send[(k + h) % n] + byte_off);
-  memcpy(out, acc, (size_t)e);
-}
-
 static void tree_value(int dtype, int op, int n, int v, const char* const* send, long long byte_off,
                        char* out) {
   const int e = esize(dtype);
@@ -141,6 +131,81 @@ static void tree_value(int dtype, int op, int n, int v, const char* const* send,
   memcpy(out, acc, (size_t)e);
 }
 
+/* Parallel bulk copy (OpenMP over 1 MiB pieces): AllGather / AllToAll
+ * blocks, the AllReduce broadcast and every single-rank collective. */
+static void pcopy(char* dst, const char* src, long long bytes) {
+  const long long piece = 1 << 20, np = (bytes + piece - 1) / piece;
+  long long p;
+#pragma omp parallel for schedule(static)
+  for (p = 0; p < np; ++p) {
+    const long long off = p * piece, len = bytes - off < piece ? bytes - off : piece;
+    memcpy(dst + off, src + off, (size_t)len);
+  }
+}
+
+/* Ring reduction of a run of m elements starting at element offset `first`,
+ * for block k: acc = x_{k+1}; acc = op(x_{k+h}, acc) for h = 2..n, with the
+ * element type's arithmetic inlined (widen, combine once, round at every
+ * hop — the same bits as combine()). */
+#define RING_RUN(T, LOAD, STORE, OPEXPR)                                       \
+  {                                                                            \
+    const T* xs[8];                                                            \
+    for (int h = 1; h <= n; ++h) xs[h - 1] = (const T*)send[(k + h) % n] + first; \
+    T* o = (T*)out;                                                            \
+    long long i;                                                               \
+    _Pragma("omp parallel for schedule(static)")                               \
+    for (i = 0; i < m; ++i) {                                                  \
+      T accr = xs[0][i];                                                       \
+      for (int h = 1; h < n; ++h) {                                            \
+        const float b = LOAD(xs[h][i]);                                        \
+        const float a = LOAD(accr);                                            \
+        accr = STORE(OPEXPR);                                                  \
+      }                                                                        \
+      o[i] = accr;                                                             \
+    }                                                                          \
+  }
+static float id_f(float x) { return x; }
+static float bf_ld(uint16_t h) { return bf16_to_f(h); }
+static float h_ld(uint16_t h) { return f16_to_f(h); }
+
+static void ring_run(int dtype, int op, int n, int k, const char* const* send, long long first, long long m,
+                     char* out) {
+  switch (dtype) {
+    case F32:
+      if (op == SUM) RING_RUN(float, id_f, id_f, b + a)
+      else if (op == MAX) RING_RUN(float, id_f, id_f, fmaxf(b, a))
+      else RING_RUN(float, id_f, id_f, fminf(b, a))
+      return;
+    case BF16:
+      if (op == SUM) RING_RUN(uint16_t, bf_ld, f_to_bf16, b + a)
+      else if (op == MAX) RING_RUN(uint16_t, bf_ld, f_to_bf16, fmaxf(b, a))
+      else RING_RUN(uint16_t, bf_ld, f_to_bf16, fminf(b, a))
+      return;
+    case F16:
+      if (op == SUM) RING_RUN(uint16_t, h_ld, f_to_f16, b + a)
+      else if (op == MAX) RING_RUN(uint16_t, h_ld, f_to_f16, fmaxf(b, a))
+      else RING_RUN(uint16_t, h_ld, f_to_f16, fminf(b, a))
+      return;
+    case I32: {
+      const int32_t* xs[8];
+      for (int h = 1; h <= n; ++h) xs[h - 1] = (const int32_t*)send[(k + h) % n] + first;
+      int32_t* o = (int32_t*)out;
+      long long i;
+#pragma omp parallel for schedule(static)
+      for (i = 0; i < m; ++i) {
+        int32_t acc = xs[0][i];
+        for (int h = 1; h < n; ++h) {
+          const int32_t b = xs[h][i];
+          acc = op == SUM ? (int32_t)((uint32_t)acc + (uint32_t)b) : op == MAX ? (acc > b ? acc : b)
+                                                                               : (acc < b ? acc : b);
+        }
+        o[i] = acc;
+      }
+      return;
+    }
+  }
+}
+
 /* Computes every rank's output. send[r] / recv[r] are host buffers sized per
  * the count semantics of include/lagom_coll.h. Returns 0, or -1 on bad args. */
 int lagom_oracle_collective(int coll, int algo, int nranks, int dtype, int op, long long count,
@@ -151,20 +216,21 @@ int lagom_oracle_collective(int coll, int algo, int nranks, int dtype, int op, l
   const int n = nranks, e = esize(dtype);
   const long long B = count;
   long long i;
+  if (n == 1) {  /* every collective of one rank is a copy of its block */
+    pcopy(recv[0], send[0], B * e);
+    return 0;
+  }
   switch (coll) {
     case AG:
       for (int r = 0; r < n; ++r)
-        for (int k = 0; k < n; ++k) memcpy(recv[r] + k * B * e, send[k], (size_t)(B * e));
+        for (int k = 0; k < n; ++k) pcopy(recv[r] + k * B * e, send[k], B * e);
       return 0;
     case A2A:
       for (int r = 0; r < n; ++r)
-        for (int q = 0; q < n; ++q) memcpy(recv[r] + q * B * e, send[q] + r * B * e, (size_t)(B * e));
+        for (int q = 0; q < n; ++q) pcopy(recv[r] + q * B * e, send[q] + r * B * e, B * e);
       return 0;
     case RS:
-      for (int r = 0; r < n; ++r) {
-#pragma omp parallel for schedule(static)
-        for (i = 0; i < B; ++i) ring_reduce(dtype, op, n, r, send, (r * B + i) * e, recv[r] + i * e);
-      }
+      for (int r = 0; r < n; ++r) ring_run(dtype, op, n, r, send, r * B, B, recv[r]);
       return 0;
     case AR: {
       if (algo == TREE) {
@@ -172,10 +238,12 @@ int lagom_oracle_collective(int coll, int algo, int nranks, int dtype, int op, l
         for (i = 0; i < B; ++i) tree_value(dtype, op, n, 0, send, i * e, recv[0] + i * e);
       } else {
         const long long blk = lagom_oracle_ring_block(B, n, dtype);
-#pragma omp parallel for schedule(static)
-        for (i = 0; i < B; ++i) ring_reduce(dtype, op, n, (int)(i / blk), send, i * e, recv[0] + i * e);
+        for (int k = 0; (long long)k * blk < B; ++k) {
+          const long long first = (long long)k * blk, m = B - first < blk ? B - first : blk;
+          ring_run(dtype, op, n, k, send, first, m, recv[0] + first * e);
+        }
       }
-      for (int r = 1; r < n; ++r) memcpy(recv[r], recv[0], (size_t)(B * e));
+      for (int r = 1; r < n; ++r) pcopy(recv[r], recv[0], B * e);
       return 0;
     }
   }

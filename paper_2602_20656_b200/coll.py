@@ -52,7 +52,8 @@ class LagomError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("max_channels", ctypes.c_int), ("steps", ctypes.c_int),
                 ("max_chunk_bytes", ctypes.c_int64), ("timeout_ms", ctypes.c_int64),
-                ("use_tma", ctypes.c_int)]
+                ("use_tma", ctypes.c_int), ("coresident", ctypes.c_int), ("one_hop", ctypes.c_int),
+                ("a2a_tma", ctypes.c_int)]
 
 
 class _Args(ctypes.Structure):
@@ -72,6 +73,7 @@ EXPORTED_SYMBOLS = (
     "lagom_comm_nvls_supported", "lagom_comm_nvls_export", "lagom_comm_nvls_import",
     "lagom_comm_nvls_bind", "lagom_comm_nvls_alloc", "lagom_comm_nvls_bytes",
     "lagom_comm_nvls_export_peer", "lagom_comm_nvls_import_peers", "lagom_comm_nvls_use_peers",
+    "lagom_coll_footprint",
 )
 
 _lib = None
@@ -116,6 +118,8 @@ def library() -> ctypes.CDLL:
         "lagom_comm_nvls_export_peer": (c_int, [vp, ctypes.c_char_p]),
         "lagom_comm_nvls_import_peers": (c_int, [vp, ctypes.c_char_p]),
         "lagom_comm_nvls_use_peers": (c_int, [vp, c_int]),
+        "lagom_coll_footprint": (c_int, [vp, ctypes.POINTER(_Args), vp, vp, ctypes.POINTER(c_int),
+                                         ctypes.POINTER(c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -179,9 +183,10 @@ class Communicator:
 
     def __init__(self, rank: int, nranks: int, device: int, *, max_channels: int = 32,
                  steps: int = 4, max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000,
-                 use_tma: int = 1):
+                 use_tma: int = 1, coresident: int = 1, one_hop: int = 0, a2a_tma: int = 0):
         lib = library()
-        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma))
+        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma), int(coresident),
+                     int(one_hop), int(a2a_tma))
         h = ctypes.c_void_p()
         _check(lib.lagom_comm_create(rank, nranks, device, ctypes.byref(opts), ctypes.byref(h)), "comm")
         self._h, self.rank, self.nranks, self.device = h, rank, nranks, device
@@ -213,26 +218,48 @@ class Communicator:
     def nvls_supported(self) -> bool:
         return bool(library().lagom_comm_nvls_supported(self._h))
 
-    def enable_nvls(self, nbytes: int, group=None) -> None:
+    def enable_nvls(self, nbytes: int, group=None, peers: bool = True) -> bool:
         """Collective: binds an NVLS multicast region of >= nbytes on every
-        rank (rank 0 creates, peers import, barrier, all bind)."""
+        rank (rank 0 creates, peers import, barrier, all bind), then maps
+        every rank's region for the one-hop schedules (``peers``).
+
+        Every step's status is agreed on by all ranks before anyone goes on,
+        so a failure on one rank raises ``LagomError`` on EVERY rank instead
+        of leaving the others blocked in the next collective. A failure of
+        the (optional) peer mappings leaves NVLS on and the one-hop schedules
+        off on every rank; returns whether they are on."""
         import torch.distributed as dist
         lib = library()
+
+        def agree(status: int, what: str) -> None:
+            got = [None] * self.nranks
+            detail = lib.lagom_last_error().decode() if status else ""
+            dist.all_gather_object(got, (status, detail), group=group)
+            bad = [(r, st, d) for r, (st, d) in enumerate(got) if st != 0]
+            if bad:
+                r, st, d = bad[0]
+                raise LagomError(_STATUS_TO_CODE.get(st, "IO_FAILURE"), "nvls",
+                                 f"{what} failed on rank {r}: {d or lib.lagom_status_string(st).decode()}", st)
+
         blob = ctypes.create_string_buffer(HANDLE_BYTES)
-        _check(lib.lagom_comm_nvls_export(self._h, nbytes, blob), "nvls")
+        agree(lib.lagom_comm_nvls_export(self._h, nbytes, blob), "multicast create/export")
         box = [blob.raw if self.rank == 0 else None]
         dist.broadcast_object_list(box, src=0, group=group)
-        _check(lib.lagom_comm_nvls_import(self._h, box[0]), "nvls")
-        dist.barrier(group=group)
-        _check(lib.lagom_comm_nvls_bind(self._h), "nvls")
-        dist.barrier(group=group)
-        # peer mappings of every rank's region (one-hop AllToAll)
-        _check(lib.lagom_comm_nvls_export_peer(self._h, blob), "nvls")
-        blobs = [None] * self.nranks
-        dist.all_gather_object(blobs, blob.raw, group=group)
-        _check(lib.lagom_comm_nvls_import_peers(self._h, b"".join(blobs)), "nvls")
-        dist.barrier(group=group)
+        agree(lib.lagom_comm_nvls_import(self._h, box[0]), "multicast import")
+        agree(lib.lagom_comm_nvls_bind(self._h), "multicast bind")
+        if not peers:
+            return False
+        # peer mappings of every rank's region (one-hop AllToAll / AG / RS)
+        st = lib.lagom_comm_nvls_export_peer(self._h, blob)
+        try:
+            agree(st, "peer export")
+            blobs = [None] * self.nranks
+            dist.all_gather_object(blobs, blob.raw, group=group)
+            agree(lib.lagom_comm_nvls_import_peers(self._h, b"".join(blobs)), "peer import")
+        except LagomError:
+            return False  # every rank got here: the one-hop schedules stay off everywhere
         _check(lib.lagom_comm_nvls_use_peers(self._h, 1), "nvls")
+        return True
 
     def nvls_alloc(self, nbytes: int) -> int:
         """Device pointer into the NVLS region (same offset on every rank when
@@ -269,6 +296,17 @@ class Communicator:
         _check(library().lagom_coll_launch(self._h, ctypes.byref(a), ctypes.c_void_p(send_ptr),
                                            ctypes.c_void_p(recv_ptr), ctypes.c_void_p(stream)), "launch")
 
+    def footprint(self, collective: int, cfg: CollConfig, dtype: int, count: int, send_ptr: int,
+                  recv_ptr: int) -> tuple[int, int]:
+        """(registers per thread, shared memory bytes per CTA) of the kernel
+        the launch would run; nothing is launched."""
+        a = make_args(collective, cfg, dtype, count)
+        regs, smem = ctypes.c_int(), ctypes.c_int()
+        _check(library().lagom_coll_footprint(self._h, ctypes.byref(a), ctypes.c_void_p(send_ptr),
+                                              ctypes.c_void_p(recv_ptr), ctypes.byref(regs), ctypes.byref(smem)),
+               "footprint")
+        return regs.value, smem.value
+
     def validate(self, collective: int, cfg: CollConfig, dtype: int = F32, count: int = 1) -> None:
         a = make_args(collective, cfg, dtype, count)
         _check(library().lagom_coll_validate(self._h, ctypes.byref(a)), "config")
@@ -296,7 +334,9 @@ class VirtualCommunicator:
     def __init__(self, nranks: int, device: int = 0, *, max_channels: int = 32, steps: int = 4,
                  max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000, use_tma: int = 1):
         lib = library()
-        opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma))
+        opts = default_opts()
+        opts.max_channels, opts.steps, opts.max_chunk_bytes = max_channels, steps, max_chunk_bytes
+        opts.timeout_ms, opts.use_tma = timeout_ms, int(use_tma)
         h = ctypes.c_void_p()
         _check(lib.lagom_comm_create_virtual(nranks, device, ctypes.byref(opts), ctypes.byref(h)), "comm")
         self._h, self.nranks, self.device = h, nranks, device

@@ -199,6 +199,7 @@ struct ReplayEngine::Impl {
   void* host_out = nullptr;  // pinned
   int calls = 0;
   bool nvls_on = false;
+  bool nvls_peers_on = false;
   std::vector<TimelineEvent> last_timeline;
 
   Impl(const ReplayDag& d, Coordinator& c, const ReplayOptions& o) : dag(d), coord(c), opts(o) {
@@ -385,6 +386,9 @@ struct ReplayEngine::Impl {
     o.max_channels = opts.max_channels;
     o.max_chunk_bytes = opts.max_chunk_bytes;
     o.use_tma = opts.use_tma ? 1 : 0;
+    o.coresident = opts.coresident ? 1 : 0;
+    o.one_hop = opts.one_hop;
+    o.a2a_tma = opts.a2a_tma ? 1 : 0;
     coll_check(lagom_comm_create(rank, n, opts.device, &o, &lcomm), "lagom_comm_create");
     if (n > 1) {
       unsigned char mine[LAGOM_HANDLE_BYTES];
@@ -428,6 +432,7 @@ struct ReplayEngine::Impl {
           pok = agree(lagom_comm_nvls_import_peers(lcomm, all.data()) == LAGOM_OK);
         }
         if (pok) coll_check(lagom_comm_nvls_use_peers(lcomm, 1), "nvls peers");
+        nvls_peers_on = pok;
         if (!pok && rank == 0 && trace_on())
           std::fprintf(stderr, "[lagom] NVLS peer mappings unavailable (%s); AllToAll stays staged\n",
                        lagom_last_error());
@@ -480,7 +485,7 @@ struct ReplayEngine::Impl {
              "cublasLtMatmul");
   }
 
-  void launch_comm_lagom(const Comm& c, const CommConfig& cfg, unsigned long long* span) {
+  lagom_coll_args_t coll_args(const Comm& c, const CommConfig& cfg, unsigned long long* span) const {
     lagom_coll_args_t a{};
     a.collective = coll_code(c.op.collective);
     a.algorithm = cfg.algorithm == Algorithm::Tree ? LAGOM_TREE : LAGOM_RING;
@@ -492,6 +497,26 @@ struct ReplayEngine::Impl {
     a.redop = LAGOM_SUM;
     a.count = c.op.count;
     a.span_out = span;
+    return a;
+  }
+
+  // Whether comm j's kernel at `cfg` fits next to a GEMM CTA on one SM
+  // (lagom_coll_footprint), cached per (op, config).
+  std::map<std::tuple<std::size_t, int, int, int, int>, bool> fits_cache;
+  bool coresident(std::size_t j, const CommConfig& cfg) {
+    const auto key = std::make_tuple(j, static_cast<int>(cfg.algorithm), static_cast<int>(cfg.protocol),
+                                     cfg.num_channels, cfg.num_threads);
+    auto it = fits_cache.find(key);
+    if (it != fits_cache.end()) return it->second;
+    const lagom_coll_args_t a = coll_args(comms[j], cfg, nullptr);
+    int regs = 0, smem = 0;
+    coll_check(lagom_coll_footprint(lcomm, &a, comms[j].send, comms[j].recv, &regs, &smem), "footprint");
+    const bool fits = regs * cfg.num_threads <= kCoresidentRegs && smem <= kCoresidentSmem;
+    return fits_cache.emplace(key, fits).first->second;
+  }
+
+  void launch_comm_lagom(const Comm& c, const CommConfig& cfg, unsigned long long* span) {
+    const lagom_coll_args_t a = coll_args(c, cfg, span);
     coll_check(lagom_coll_launch(lcomm, &a, c.send, c.recv, ks), c.op.id.c_str());
   }
 
@@ -522,7 +547,9 @@ struct ReplayEngine::Impl {
     }
   }
 
-  // One replay on this rank; returns [x_0..x_{N-1}, y_0..y_{M-1}, Z] in us.
+  // One replay on this rank; returns [x_0..x_{N-1}, y_0..y_{M-1}, Z,
+  // xev_0..xev_{N-1}] in us (x: kernel span for Lagom kernels, else events;
+  // xev: events).
   std::vector<double> replay(Mode mode, const std::vector<CommConfig>* cfgs) {
     const bool do_compute = mode != Mode::CommOnly;
     const bool do_comm = mode != Mode::ComputeOnly;
@@ -534,11 +561,18 @@ struct ReplayEngine::Impl {
     // no collective can overlap (e.g. before the first gate) keep the whole
     // GPU, and collectives gated on the last op cost the GEMMs nothing.
     std::vector<int> sm_target(M, 0);
-    if (opts.reserve_comm_sms && cfgs && (mode == Mode::Lagom || mode == Mode::LagomE2E)) {
+    const bool lagom_part =
+        opts.sm_partition != kPartitionNone && cfgs && (mode == Mode::Lagom || mode == Mode::LagomE2E);
+    const bool nccl_part = opts.nccl_reserve_sms > 0 && mode == Mode::Nccl;
+    if (lagom_part || nccl_part) {
       std::vector<int> reserve(M, 0);
-      for (std::size_t j = 0; j < N; ++j)
+      for (std::size_t j = 0; j < N; ++j) {
+        const int r = nccl_part ? opts.nccl_reserve_sms
+                      : (opts.sm_partition == kPartitionAll || !coresident(j, (*cfgs)[j])) ? (*cfgs)[j].num_channels
+                                                                                          : 0;
         for (std::size_t i = static_cast<std::size_t>(comms[j].dep + 1); i < M; ++i)
-          reserve[i] = std::max(reserve[i], (*cfgs)[j].num_channels);
+          reserve[i] = std::max(reserve[i], r);
+      }
       for (std::size_t i = 0; i < M; ++i)
         if (reserve[i] > 0) sm_target[i] = std::max(1, num_sms - reserve[i]);
     }
@@ -582,7 +616,7 @@ struct ReplayEngine::Impl {
     cuda_check(cudaEventSynchronize(ev_kend), "sync");
     coll_check(lagom_comm_check(lcomm), "collective watchdog");
 
-    std::vector<double> out(N + M + 1, 0.0);
+    std::vector<double> out(N + M + 1 + N, 0.0);
     auto us = [](cudaEvent_t a, cudaEvent_t b) {
       float ms = 0.f;
       cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
@@ -590,7 +624,7 @@ struct ReplayEngine::Impl {
     };
     double z = 0.0;
     if (do_comm)
-      for (std::size_t j = 0; j < N; ++j) out[j] = us(ev_kb[j], ev_ke[j]);
+      for (std::size_t j = 0; j < N; ++j) out[j] = out[N + M + 1 + j] = us(ev_kb[j], ev_ke[j]);
     if (spans_on) {
       // x_j = the kernel's active span (first CTA start .. last CTA end):
       // excludes time the launch sat queued behind persistent GEMM CTAs.
@@ -651,6 +685,8 @@ struct ReplayEngine::Impl {
     m.profile.total_compute = 0.0;
     for (double y : m.comp_times) m.profile.total_compute += y;
     m.profile.makespan = med(N + M);
+    m.comm_event_times.resize(N);
+    for (std::size_t j = 0; j < N; ++j) m.comm_event_times[j] = med(N + M + 1 + j);
     m.timeline = last_timeline;
     ++calls;
     m.wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
@@ -667,6 +703,8 @@ struct ReplayEngine::Impl {
     wire[0].algorithm = static_cast<std::int32_t>(mode);
     wire[0].protocol = opts.repeats;  // measurement settings travel with the command
     wire[0].transport = opts.warmup;
+    wire[0].num_channels = opts.sm_partition;
+    wire[0].num_threads = opts.nccl_reserve_sms;
     if (cfgs) {
       if (cfgs->size() != comms.size())
         throw Error(ErrorCode::InvalidWorkload, "configs", "one config per comm op expected");
@@ -695,6 +733,14 @@ void ReplayEngine::set_measurement(int repeats, int warmup) {
   impl_->opts.repeats = std::max(1, repeats);
   impl_->opts.warmup = std::max(0, warmup);
 }
+void ReplayEngine::set_partition(int sm_partition, int nccl_reserve_sms) {
+  if (sm_partition < kPartitionNone || sm_partition > kPartitionAll)
+    throw Error(ErrorCode::InvalidInput, "sm_partition", "must be 0 (none), 1 (auto) or 2 (all)");
+  impl_->opts.sm_partition = sm_partition;
+  impl_->opts.nccl_reserve_sms = std::max(0, std::min(nccl_reserve_sms, impl_->num_sms - 1));
+}
+bool ReplayEngine::nvls_active() const { return impl_->nvls_on; }
+bool ReplayEngine::nvls_peers_active() const { return impl_->nvls_peers_on; }
 
 ReplayMeasurement ReplayEngine::run(const std::vector<CommConfig>& configs) {
   return impl_->measure(Mode::Lagom, &configs);
@@ -725,6 +771,8 @@ void ReplayEngine::serve() {
       cfgs[j] = CommConfig{static_cast<Algorithm>(w.algorithm), static_cast<Protocol>(w.protocol),
                            static_cast<Transport>(w.transport), w.num_channels, w.num_threads, w.chunk_size};
     }
+    I.opts.sm_partition = wire[0].num_channels;
+    I.opts.nccl_reserve_sms = wire[0].num_threads;
     const bool with_cfg = mode == Mode::Lagom || mode == Mode::CommOnly || mode == Mode::LagomE2E;
     I.measure(mode, with_cfg ? &cfgs : nullptr, wire[0].protocol, wire[0].transport);
   }

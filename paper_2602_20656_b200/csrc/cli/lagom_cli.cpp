@@ -346,7 +346,7 @@ std::optional<lagom::TuneResult> tune_on_gpu(const Args& a, const lagom::Workloa
   auto coord = lagom::b200::make_shm_coordinator(name, rank, world);
   lagom::b200::ReplayOptions o;
   o.device = local;
-  o.reserve_comm_sms = true;
+  o.sm_partition = lagom::b200::kPartitionAuto;
   o.enable_nccl = false;
   lagom::b200::ReplayEngine engine(dag, *coord, o);
   if (rank != 0) {

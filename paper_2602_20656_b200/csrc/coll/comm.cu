@@ -40,10 +40,25 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
   } while (0)
 
+// Heap header: the options every rank must agree on (they select kernels
+// and the heap layout), written at creation, compared at import.
+struct HeapHeader {
+  uint64_t magic;
+  int64_t nranks, max_channels, steps, max_chunk_bytes, use_tma, coresident, one_hop, a2a_tma;
+};
+constexpr uint64_t kHeapMagic = 0x4c41474f4d484452ull;  // "LAGOMHDR"
+
+HeapHeader header_of(const lagom_comm* c) {
+  return HeapHeader{kHeapMagic, c->nranks, c->opts.max_channels, c->opts.steps, c->opts.max_chunk_bytes,
+                    c->opts.use_tma, c->opts.coresident, c->opts.one_hop, c->opts.a2a_tma};
+}
+
 void layout(lagom_comm* c) {
   const int64_t n = c->nranks, ch = c->opts.max_channels;
   c->slot_bytes = 2 * c->opts.max_chunk_bytes;  // LL doubles the payload
   int64_t off = 0;
+  c->off_hdr = off;
+  off += 256;
   c->off_ready = off;
   off += ch * n * 128;
   c->off_freed = off;
@@ -69,6 +84,10 @@ int check_opts(lagom_comm_opts_t* o) {
   if (o->max_chunk_bytes < 1024 || o->max_chunk_bytes % 1024 != 0)
     return fail(LAGOM_ERR_INVALID_ARGUMENT, "max_chunk_bytes must be a positive 1 KiB multiple");
   if (o->timeout_ms < 1) return fail(LAGOM_ERR_INVALID_ARGUMENT, "timeout_ms must be >= 1");
+  if (o->use_tma < 0 || o->use_tma > 2) return fail(LAGOM_ERR_INVALID_ARGUMENT, "use_tma must be 0, 1 or 2");
+  if (o->coresident < 0 || o->coresident > 1) return fail(LAGOM_ERR_INVALID_ARGUMENT, "coresident must be 0 or 1");
+  if (o->one_hop < 0 || o->one_hop > 2) return fail(LAGOM_ERR_INVALID_ARGUMENT, "one_hop must be 0, 1 or 2");
+  if (o->a2a_tma < 0 || o->a2a_tma > 1) return fail(LAGOM_ERR_INVALID_ARGUMENT, "a2a_tma must be 0 or 1");
   return LAGOM_OK;
 }
 
@@ -77,6 +96,9 @@ int alloc_common(lagom_comm* c) {
   LAGOM_CUDA(cudaHostAlloc(&c->abort_host, sizeof(unsigned int), cudaHostAllocMapped));
   *c->abort_host = 0;
   LAGOM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->abort_dev), c->abort_host, 0));
+  cudaEvent_t ev;
+  LAGOM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  c->order_ev = ev;
   return LAGOM_OK;
 }
 
@@ -198,6 +220,9 @@ KParams make_params(const lagom_comm* c, const lagom_coll_args_t* a) {
   return p;
 }
 
+int launch_real(lagom_comm* c, const lagom_coll_args_t* a, const void* sendbuf, void* recvbuf, cudaStream_t stream);
+int select_real(lagom_comm* c, const lagom_coll_args_t* a, const void* sendbuf, void* recvbuf, LaunchPlan* plan);
+
 }  // namespace
 
 extern "C" {
@@ -225,6 +250,9 @@ void lagom_comm_default_opts(lagom_comm_opts_t* o) {
   o->max_chunk_bytes = 4 << 20;
   o->timeout_ms = 10000;
   o->use_tma = 1;
+  o->coresident = 1;
+  o->one_hop = 0;
+  o->a2a_tma = 0;
 }
 
 int lagom_comm_create(int rank, int nranks, int device, const lagom_comm_opts_t* opts,
@@ -243,10 +271,13 @@ int lagom_comm_create(int rank, int nranks, int device, const lagom_comm_opts_t*
   void* h = nullptr;
   cudaError_t e = cudaMalloc(&h, static_cast<size_t>(c->heap_bytes));
   if (e == cudaSuccess) e = cudaMemset(h, 0, static_cast<size_t>(c->heap_bytes));
+  const HeapHeader hdr = header_of(c);
+  if (e == cudaSuccess) e = cudaMemcpy(static_cast<char*>(h) + c->off_hdr, &hdr, sizeof hdr, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (h) cudaFree(h);
     cudaFreeHost(c->abort_host);
+    if (c->order_ev) cudaEventDestroy(static_cast<cudaEvent_t>(c->order_ev));
     delete c;
     return cuda_fail(e, "heap allocation");
   }
@@ -278,6 +309,17 @@ int lagom_comm_import_handles(lagom_comm_t c, const void* handles) {
     LAGOM_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     c->heap[r] = static_cast<char*>(p);
     c->imported[r] = true;
+  }
+  // every peer must have been created with the same kernel-selecting options
+  const HeapHeader mine = header_of(c);
+  for (int r = 0; r < c->nranks; ++r) {
+    if (r == c->rank) continue;
+    HeapHeader peer{};
+    LAGOM_CUDA(cudaMemcpy(&peer, c->heap[r] + c->off_hdr, sizeof peer, cudaMemcpyDefault));
+    if (std::memcmp(&peer, &mine, sizeof mine) != 0)
+      return fail(LAGOM_ERR_INVALID_ARGUMENT,
+                  "rank " + std::to_string(r) + " was created with different options (nranks, max_channels, steps, "
+                  "max_chunk_bytes, use_tma, coresident, one_hop, a2a_tma must match on every rank)");
   }
   c->ready = true;
   return LAGOM_OK;
@@ -324,6 +366,7 @@ int lagom_comm_destroy(lagom_comm_t c) {
   }
   lagom_nvls_release(c);
   if (c->abort_host) cudaFreeHost(c->abort_host);
+  if (c->order_ev) cudaEventDestroy(static_cast<cudaEvent_t>(c->order_ev));
   delete c;
   return LAGOM_OK;
 }
@@ -361,30 +404,54 @@ int lagom_coll_launch(lagom_comm_t c, const lagom_coll_args_t* a, const void* se
     return fail(LAGOM_ERR_BROKEN, "communicator broken by an earlier abort");
   }
   if (a->count == 0) return LAGOM_OK;
+  // Issue order across streams: this launch waits for the previous one on
+  // this communicator (they share step counters, slots and NVLS epochs).
+  const auto st = static_cast<cudaStream_t>(stream);
+  const auto order = static_cast<cudaEvent_t>(c->order_ev);
+  LAGOM_CUDA(cudaStreamWaitEvent(st, order, 0));
+  const int s = launch_real(c, a, sendbuf, recvbuf, st);
+  if (s != LAGOM_OK) return s;
+  LAGOM_CUDA(cudaEventRecord(order, st));
+  return LAGOM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int select_real(lagom_comm* c, const lagom_coll_args_t* a, const void* sendbuf, void* recvbuf, LaunchPlan* plan) {
+  if (c->nranks == 1) return lagom_local_select(c, a, sendbuf, recvbuf, plan);
   {  // TREE on an NVSwitch box with NVLS bound: the switch-rooted schedule
-    alignas(16) unsigned char nv[512];
     size_t nv_bytes = 0;
-    const void* nk = nullptr;
-    int nsmem = 0;
-    if (lagom_nvls_prepare(c, a, sendbuf, recvbuf, &nk, nv, &nv_bytes, &nsmem) == 1) {
-      void* nargs[] = {nv};
-      LAGOM_CUDA(cudaLaunchKernel(nk, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), nargs,
-                                  static_cast<size_t>(nsmem), static_cast<cudaStream_t>(stream)));
-      return LAGOM_OK;
-    }
+    const int prep = lagom_nvls_prepare(c, a, sendbuf, recvbuf, &plan->kernel, plan->params, &nv_bytes, &plan->smem);
+    if (prep < 0) return LAGOM_ERR_INVALID_ARGUMENT;  // reason recorded by lagom_nvls_prepare
+    if (prep == 1) return LAGOM_OK;
   }
   KParams p = make_params(c, a);
   p.send[0] = static_cast<const char*>(sendbuf);
   p.recv[0] = static_cast<char*>(recvbuf);
+  static_assert(sizeof p <= sizeof plan->params, "launch plan too small");
   const void* k = pick_kernel(a);
   if (!k) return fail(LAGOM_ERR_INVALID_ARGUMENT, "no kernel for this combination");
-  void* args[] = {&p};
   const int smem = smem_for(p, a, k);
   if (smem < 0) return fail(LAGOM_ERR_CUDA, "cannot enable the TMA shared-memory ring");
-  LAGOM_CUDA(cudaLaunchKernel(k, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), args,
-                              static_cast<size_t>(smem), static_cast<cudaStream_t>(stream)));
+  std::memcpy(plan->params, &p, sizeof p);
+  plan->kernel = k;
+  plan->smem = smem;
   return LAGOM_OK;
 }
+
+int launch_real(lagom_comm* c, const lagom_coll_args_t* a, const void* sendbuf, void* recvbuf, cudaStream_t stream) {
+  LaunchPlan plan;
+  if (int s = select_real(c, a, sendbuf, recvbuf, &plan)) return s;
+  if (!plan.kernel) return LAGOM_OK;
+  void* args[] = {plan.params};
+  LAGOM_CUDA(cudaLaunchKernel(plan.kernel, dim3(a->num_channels, 1, 1), dim3(a->num_threads, 1, 1), args,
+                              static_cast<size_t>(plan.smem), stream));
+  return LAGOM_OK;
+}
+}  // namespace
+
+extern "C" {
 
 int lagom_coll_launch_virtual(lagom_comm_t c, const lagom_coll_args_t* a,
                               const void* const* sendbufs, void* const* recvbufs, void* stream) {
@@ -407,9 +474,30 @@ int lagom_coll_launch_virtual(lagom_comm_t c, const lagom_coll_args_t* a,
   if (smem < 0) return fail(LAGOM_ERR_CUDA, "cannot enable the TMA shared-memory ring");
   // Ranks spin on one another: a cooperative launch guarantees that every
   // rank's CTAs are co-resident (or fails loudly instead of hanging).
+  const auto st = static_cast<cudaStream_t>(stream);
+  const auto order = static_cast<cudaEvent_t>(c->order_ev);
+  LAGOM_CUDA(cudaStreamWaitEvent(st, order, 0));
   LAGOM_CUDA(cudaLaunchCooperativeKernel(k, dim3(a->num_channels, c->nranks, 1),
-                                         dim3(a->num_threads, 1, 1), args, static_cast<size_t>(smem),
-                                         static_cast<cudaStream_t>(stream)));
+                                         dim3(a->num_threads, 1, 1), args, static_cast<size_t>(smem), st));
+  LAGOM_CUDA(cudaEventRecord(order, st));
+  return LAGOM_OK;
+}
+
+int lagom_coll_footprint(lagom_comm_t c, const lagom_coll_args_t* a, const void* sendbuf, void* recvbuf,
+                         int* regs_per_thread, int* smem_bytes) {
+  if (int s = validate(c, a)) return s;
+  if (c->virt) return fail(LAGOM_ERR_INVALID_ARGUMENT, "footprint needs a real-mode comm");
+  if (!regs_per_thread || !smem_bytes) return fail(LAGOM_ERR_INVALID_ARGUMENT, "null output");
+  *regs_per_thread = 0;
+  *smem_bytes = 0;
+  if (a->count == 0) return LAGOM_OK;
+  LaunchPlan plan;
+  if (int s = select_real(c, a, sendbuf, recvbuf, &plan)) return s;
+  if (!plan.kernel) return LAGOM_OK;
+  cudaFuncAttributes fa;
+  LAGOM_CUDA(cudaFuncGetAttributes(&fa, plan.kernel));
+  *regs_per_thread = fa.numRegs;
+  *smem_bytes = static_cast<int>(fa.sharedSizeBytes) + plan.smem;
   return LAGOM_OK;
 }
 

@@ -21,6 +21,8 @@ struct lagom_comm {
   unsigned int* abort_host = nullptr;
   unsigned int* abort_dev = nullptr;
   bool broken = false;
+  void* order_ev = nullptr;                 // cudaEvent_t: the last launch (issue order)
+  int64_t off_hdr = 0;                      // heap header: options peers must agree on
   // NVLS (NVLink SHARP multicast): a symmetric region bound to a multicast
   // object spanning every rank's GPU (nvls.cu).
   unsigned long long nvls_mc_handle = 0;    // CUmemGenericAllocationHandle (multicast)
@@ -42,3 +44,13 @@ struct lagom_comm {
 
 // Records `what` as lagom_last_error() and returns `status`.
 int lagom_fail(int status, const std::string& what);
+// One launch, decided but not issued: kernel (nullptr = nothing to launch),
+// its single by-value parameter block, dynamic shared memory.
+struct LaunchPlan {
+  const void* kernel = nullptr;
+  alignas(16) unsigned char params[512];
+  int smem = 0;
+};
+// nranks == 1: the copy kernel of local.cu (no launch in place).
+int lagom_local_select(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
+                       LaunchPlan* plan);

@@ -169,8 +169,12 @@ __device__ __forceinline__ void mm_store(void* p, uint4 v) {
                : "memory");
 }
 
-template <int KIND, typename T, int U, int MAXT>
-__global__ void __launch_bounds__(MAXT) nvls_kernel(const __grid_constant__ NvlsParams P) {
+// MINB = 3 (co-resident variants): <= 65536 / (3 x MAXT) registers per
+// thread, i.e. <= 21.8 K registers per CTA at NT = MAXT, which fits next to
+// an sm_100 cuBLASLt GEMM CTA (256 x 168 registers, ~214 KB shared memory)
+// on one SM. MINB = 1: the deep-unroll variants of round 1.
+template <int KIND, typename T, int U, int MAXT, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant__ NvlsParams P) {
   __shared__ int s_ok;
   const int ch = blockIdx.x, nch = gridDim.x, n = P.nranks, r = P.rank;
   if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
@@ -420,35 +424,40 @@ __global__ void __launch_bounds__(640) a2a_tma_kernel(const __grid_constant__ Nv
   }
 }
 
-template <int KIND, int U, int MAXT>
+template <int KIND, int U, int MAXT, int MINB = 1>
 const void* pick_nvls_u(int dtype) {
+  // the copy kinds (AG, A2A, one-hop AG) move bytes: one instantiation
+  if (KIND == 1 || KIND == 3 || KIND == 4)
+    return reinterpret_cast<const void*>(&nvls_kernel<KIND, int32_t, U, MAXT, MINB>);
   switch (dtype) {
-    case LAGOM_F32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, float, U, MAXT>);
-    case LAGOM_BF16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __nv_bfloat16, U, MAXT>);
-    case LAGOM_F16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __half, U, MAXT>);
-    case LAGOM_I32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, int32_t, U, MAXT>);
+    case LAGOM_F32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, float, U, MAXT, MINB>);
+    case LAGOM_BF16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __nv_bfloat16, U, MAXT, MINB>);
+    case LAGOM_F16: return reinterpret_cast<const void*>(&nvls_kernel<KIND, __half, U, MAXT, MINB>);
+    case LAGOM_I32: return reinterpret_cast<const void*>(&nvls_kernel<KIND, int32_t, U, MAXT, MINB>);
   }
   return nullptr;
 }
 // Requests in flight per thread. multimem.ld_reduce is a round trip through
 // the switch, so AR / RS throughput per SM is set by the bytes in flight,
 // NT x U x 16 B (measured on 4xB200: AR 25 MiB at NC = 4, NT = 512 goes from
-// 232 to 411 GB/s busbw with U = 16 instead of 8). Small CTAs (the Lagom
-// search starts at NT = 64) get a deeper unroll so they are not starved:
-// NT <= 256 -> U = 32 (128 data registers, launch bound 256); else U = 16.
-// Large-NT AG only needs U = 8 (its loads are local). LAGOM_NVLS_UNROLL = 4 | 8 | 16 forces one
-// unroll at every NT (experiments).
+// 232 to 411 GB/s busbw with U = 16 instead of 8).
+//   coresident: per thread-count class, U such that NT x U x 16 B ~ 32 KB
+//     (64: 32, 128: 16, 256: 8, 384..640: 4) under the 21.8 K-register CTA
+//     budget; one-hop RS (acc[U] + v[U]) takes half.
+//   otherwise (round 1): NT <= 256 -> U = 32 (launch bound 256); else U = 16
+//     (U = 8 for the copy kinds).
 template <int KIND>
-const void* pick_nvls(int dtype, int nt) {
-  static const int forced = [] {
-    const char* e = std::getenv("LAGOM_NVLS_UNROLL");
-    const int v = e ? std::atoi(e) : 0;
-    return (v == 4 || v == 8 || v == 16) ? v : 0;
-  }();
-  switch (forced) {
-    case 4: return pick_nvls_u<KIND, 4, 640>(dtype);
-    case 8: return pick_nvls_u<KIND, 8, 640>(dtype);
-    case 16: return pick_nvls_u<KIND, 16, 640>(dtype);
+const void* pick_nvls(int dtype, int nt, bool coresident) {
+  if (coresident) {
+    // one-hop RS (acc + v) and the A2A (a peer pointer per step): half the
+    // unroll where the full one would spill under the register cap
+    constexpr int H = KIND == 5 ? 2 : 1, H3 = KIND == 3 ? 2 : 1;
+    if (nt <= 64) return pick_nvls_u<KIND, 32 / H / H3, 64, 3>(dtype);
+    if (nt <= 128) return pick_nvls_u<KIND, 16 / H, 128, 3>(dtype);
+    if (nt <= 256) return pick_nvls_u<KIND, 8 / H, 256, 3>(dtype);
+    if (nt <= 384) return pick_nvls_u<KIND, 4 / H, 384, 3>(dtype);
+    if (nt <= 512) return pick_nvls_u<KIND, 4 / H / H3, 512, 3>(dtype);
+    return pick_nvls_u<KIND, 4 / H / H3, 640, 3>(dtype);
   }
   if (KIND == 5)  // one-hop RS holds acc[U] + v[U]: half the unroll of ld_reduce
     return nt <= 256 ? pick_nvls_u<KIND, 16, 256>(dtype) : pick_nvls_u<KIND, 8, 640>(dtype);
@@ -465,33 +474,21 @@ int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 :
 
 }  // namespace
 
-// Used by lagom_coll_launch: 1 if this launch can run on the switch, with
-// *kernel/params filled in; 0 to fall back to the P2P kernels.
+// Used by lagom_coll_launch: 1 if this launch runs on the switch / the peer
+// mappings, with *kernel/params filled in; 0 to run the P2P kernels; -1 (with
+// lagom_last_error set) if it must run there but cannot.
+//
 // TREE AllGather / ReduceScatter through the peer mappings (peer stores /
-// peer loads) instead of the switch. At n = 2 the multicast echo of the own
-// block caps NVLS AllGather and ReduceScatter at ~330 GB/s busbw from NC = 8
-// upward, while the one-hop schedules keep scaling with the channels
-// (AllGather on a 4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355 vs 278;
-// NC 32: 569 vs 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl).
-// LAGOM_ONE_HOP=2 follows the config (one hop at n = 2 and NC >= 12, the
-// switch otherwise; every rank launches the same config, so every rank makes
-// the same choice), 1 forces one hop, 0 / unset keeps the switch — the
-// default, see DESIGN.md §6 for the FSDP replay at n = 2.
-bool one_hop(int n, int nc) {
-  static const int mode = [] {
-    const char* e = std::getenv("LAGOM_ONE_HOP");
-    return e && *e ? std::atoi(e) : 0;
-  }();
-  return mode == 1 || (mode == 2 && n == 2 && nc >= 12);
-}
-
-// LAGOM_A2A_TMA=0 selects the LSU (vector ld/st) one-hop AllToAll.
-bool a2a_use_tma() {
-  static const bool on = [] {
-    const char* e = std::getenv("LAGOM_A2A_TMA");
-    return !(e && *e == '0');
-  }();
-  return on;
+// peer loads) instead of the switch (opts.one_hop). At n = 2 the multicast
+// echo of the own block caps NVLS AllGather and ReduceScatter at ~330 GB/s
+// busbw from NC = 8 upward, while the one-hop schedules keep scaling with the
+// channels (AllGather on a 4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355
+// vs 278; NC 32: 569 vs 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl).
+// one_hop = 2 follows the config (one hop at n = 2 and NC >= 12; every rank
+// launches the same config, so every rank makes the same choice).
+bool one_hop(const lagom_comm* c, int nc) {
+  const int mode = c->opts.one_hop;
+  return c->nvls_peers_ready && (mode == 1 || (mode == 2 && c->nranks == 2 && nc >= 12));
 }
 
 int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
@@ -499,26 +496,25 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   *smem_bytes = 0;
   if (!c->nvls_ready || a->algorithm != LAGOM_TREE || a->redop != LAGOM_SUM || c->virt) return 0;
   const int64_t e = ebytes(a->dtype), n = c->nranks;
+  const bool co = c->opts.coresident != 0, hop = one_hop(c, a->num_channels);
   int64_t in_b = 0, out_b = 0;
   const void* k = nullptr;
   switch (a->collective) {
-    case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype, a->num_threads); break;
+    case LAGOM_ALL_REDUCE: in_b = out_b = a->count * e; k = pick_nvls<0>(a->dtype, a->num_threads, co); break;
     case LAGOM_ALL_GATHER:
       in_b = a->count * e;
       out_b = a->count * e * n;
-      k = (c->nvls_peers_ready && one_hop(c->nranks, a->num_channels)) ? pick_nvls<4>(a->dtype, a->num_threads)
-                                                         : pick_nvls<1>(a->dtype, a->num_threads);
+      k = hop ? pick_nvls<4>(a->dtype, a->num_threads, co) : pick_nvls<1>(a->dtype, a->num_threads, co);
       break;
     case LAGOM_REDUCE_SCATTER:
       in_b = a->count * e * n;
       out_b = a->count * e;
-      k = (c->nvls_peers_ready && one_hop(c->nranks, a->num_channels)) ? pick_nvls<5>(a->dtype, a->num_threads)
-                                                                      : pick_nvls<2>(a->dtype, a->num_threads);
+      k = hop ? pick_nvls<5>(a->dtype, a->num_threads, co) : pick_nvls<2>(a->dtype, a->num_threads, co);
       break;
     case LAGOM_ALL_TO_ALL:
       if (!c->nvls_peers_ready) return 0;
       in_b = out_b = a->count * e * n;
-      if (a2a_use_tma()) {
+      if (c->opts.a2a_tma) {
         static const bool smem_ok =
             cudaFuncSetAttribute(reinterpret_cast<const void*>(&a2a_tma_kernel),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
@@ -528,18 +524,28 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
           break;
         }
       }
-      k = pick_nvls<3>(a->dtype, a->num_threads);
+      k = pick_nvls<3>(a->dtype, a->num_threads, co);
       break;
     default: return 0;
   }
-  if ((a->count * e) % 16 != 0) return 0;  // whole 16 B units per block
-  // peer-store kernels (one-hop AllToAll / AllGather) write into peer_recv
-  const bool a2a = a->collective == LAGOM_ALL_TO_ALL ||
-                   (a->collective == LAGOM_ALL_GATHER && c->nvls_peers_ready && one_hop(c->nranks, a->num_channels));
+  // Whole 16 B units per block: a property of (collective, count, dtype),
+  // identical on every rank, so every rank falls back to P2P together.
+  if ((a->count * e) % 16 != 0) return 0;
+  // peer-store kernels (one-hop AllToAll / AllGather) write into peer_recv,
+  // the one-hop RS reads peer_send: both buffers must be in the region too
+  const bool a2a = a->collective == LAGOM_ALL_TO_ALL || (a->collective == LAGOM_ALL_GATHER && hop);
   const bool send_mc = a->collective != LAGOM_ALL_GATHER && !a2a, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
-  if ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15) return 0;
-  if (send_mc && !inside(c, send, in_b)) return 0;
-  if (recv_mc && !inside(c, recv, out_b)) return 0;
+  const bool need_send = send_mc || (a->collective == LAGOM_REDUCE_SCATTER && hop);
+  const bool need_recv = recv_mc || a2a;
+  // Buffer placement is per rank: a rank that fell back to P2P here while
+  // its peers ran the switch kernel would wait on flags nobody writes, so a
+  // misplaced buffer is an error, not a fallback.
+  if ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15)
+    return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "TREE with NVLS bound: buffers must be 16-byte aligned"), -1;
+  if ((need_send && !inside(c, send, in_b)) || (need_recv && !inside(c, recv, out_b)))
+    return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT,
+                      "TREE with NVLS bound: send/recv must lie in the NVLS region (lagom_comm_nvls_alloc)"),
+           -1;
   NvlsParams p{};
   for (int r = 0; r < c->nranks; ++r) p.heap[r] = c->heap[r];
   p.rank = c->rank;
@@ -552,7 +558,7 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   p.recv_mc = recv_mc && !a2a ? c->nvls_mc + (static_cast<char*>(recv) - c->nvls_uc) : nullptr;
   if (a2a)
     for (int q = 0; q < c->nranks; ++q) p.peer_recv[q] = c->nvls_peer[q] + (static_cast<char*>(recv) - c->nvls_uc);
-  if (a->collective == LAGOM_REDUCE_SCATTER && c->nvls_peers_ready && one_hop(c->nranks, a->num_channels))
+  if (a->collective == LAGOM_REDUCE_SCATTER && hop)
     for (int q = 0; q < c->nranks; ++q)
       p.peer_send[q] = c->nvls_peer[q] + (static_cast<const char*>(send) - c->nvls_uc);
   p.off_nvbar = c->off_nvbar;

@@ -137,7 +137,7 @@ GpuSpec gpu_from_json(const std::string& s) {
 Json measurement_json(const b200::ReplayMeasurement& m) {
   SimResult tl;
   tl.timeline = m.timeline;
-  return Json{{"x", m.profile.comm_times}, {"y", m.comp_times}, {"X", m.profile.total_comm},
+  return Json{{"x", m.profile.comm_times}, {"x_ev", m.comm_event_times}, {"y", m.comp_times}, {"X", m.profile.total_comm},
               {"Y", m.profile.total_compute}, {"Z", m.profile.makespan}, {"wall_us", m.wall_us},
               {"trace", trace_to_json(tl)}};
 }
@@ -148,7 +148,8 @@ class PyEngine {
  public:
   PyEngine(const std::string& dag_json, const std::string& coord_name, int rank, int size, int device,
            int repeats, int warmup, bool nccl, std::int64_t max_chunk, int max_channels,
-           std::int64_t e2e_in, std::int64_t e2e_out, bool reserve, bool nvls)
+           std::int64_t e2e_in, std::int64_t e2e_out, int sm_partition, bool nvls, bool coresident, int one_hop,
+           bool a2a_tma)
       : dag_(dag_from_json(parse(dag_json))) {
     coord_ = b200::make_shm_coordinator(coord_name, rank, size);
     b200::ReplayOptions o;
@@ -160,8 +161,11 @@ class PyEngine {
     o.max_channels = max_channels;
     o.e2e_in_bytes = e2e_in;
     o.e2e_out_bytes = e2e_out;
-    o.reserve_comm_sms = reserve;
+    o.sm_partition = sm_partition;
     o.nvls = nvls;
+    o.coresident = coresident;
+    o.one_hop = one_hop;
+    o.a2a_tma = a2a_tma;
     engine_ = std::make_unique<b200::ReplayEngine>(dag_, *coord_, o);
   }
   std::string workload(const std::string& gpu_json) const {
@@ -225,6 +229,9 @@ class PyEngine {
     engine_.reset();
   }
   void set_measurement(int repeats, int warmup) { engine_->set_measurement(repeats, warmup); }
+  void set_partition(int sm_partition, int nccl_reserve) { engine_->set_partition(sm_partition, nccl_reserve); }
+  bool nvls_active() const { return engine_->nvls_active(); }
+  bool nvls_peers_active() const { return engine_->nvls_peers_active(); }
   int rank() const { return engine_->rank(); }
   int nranks() const { return engine_->nranks(); }
   void barrier() {
@@ -336,11 +343,12 @@ PYBIND11_MODULE(_lagom_py, m) {
 
   py::class_<PyEngine>(m, "ReplayEngine")
       .def(py::init<const std::string&, const std::string&, int, int, int, int, int, bool, std::int64_t, int,
-                    std::int64_t, std::int64_t, bool, bool>(),
+                    std::int64_t, std::int64_t, int, bool, bool, int, bool>(),
            py::arg("dag"), py::arg("coord_name"), py::arg("rank"), py::arg("size"), py::arg("device"),
            py::arg("repeats") = 3, py::arg("warmup") = 1, py::arg("nccl") = true,
            py::arg("max_chunk_bytes") = 4 << 20, py::arg("max_channels") = 32, py::arg("e2e_in_bytes") = 0,
-           py::arg("e2e_out_bytes") = 0, py::arg("reserve_comm_sms") = false, py::arg("nvls") = false)
+           py::arg("e2e_out_bytes") = 0, py::arg("sm_partition") = 1, py::arg("nvls") = false,
+           py::arg("coresident") = true, py::arg("one_hop") = 0, py::arg("a2a_tma") = false)
       .def("workload", &PyEngine::workload, py::arg("gpu") = "")
       .def("run", &PyEngine::run)
       .def("run_e2e", &PyEngine::run_e2e)
@@ -354,6 +362,9 @@ PYBIND11_MODULE(_lagom_py, m) {
       .def("close", &PyEngine::close)
       .def("set_measurement", &PyEngine::set_measurement, py::arg("repeats"), py::arg("warmup") = 0)
       .def("barrier", &PyEngine::barrier)
+      .def("set_partition", &PyEngine::set_partition, py::arg("sm_partition"), py::arg("nccl_reserve_sms") = 0)
+      .def_property_readonly("nvls_active", &PyEngine::nvls_active)
+      .def_property_readonly("nvls_peers_active", &PyEngine::nvls_peers_active)
       .def_property_readonly("rank", &PyEngine::rank)
       .def_property_readonly("nranks", &PyEngine::nranks);
 }

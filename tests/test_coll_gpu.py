@@ -160,3 +160,74 @@ def test_zero_count_is_a_no_op(vcomms):
     for coll in range(4):
         vcomms[2].launch(coll, C.CollConfig(C.RING, C.SIMPLE, 2, 64, 32768), C.F32, 0, [0, 0], [0, 0])
     vcomms[2].check()
+
+
+NT_CLASSES = [64, 128, 192, 256, 384, 512, 576, 640]
+
+
+@pytest.mark.parametrize("nt", NT_CLASSES)
+@pytest.mark.parametrize("coll", [0, 1, 2, 3])
+def test_single_rank_real_mode_is_a_copy(coll, nt):
+    """nranks == 1 (the bench's N = 1 line): every collective is a copy of
+    count elements through the co-resident copy kernel (local.cu), bit-exact
+    against the oracle at n = 1, for every thread-count class, with src/dst
+    co-aligned, mutually misaligned, and ragged byte counts."""
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    import torch
+    from paper_2602_20656_b200 import coll as C
+    comm = C.Communicator(0, 1, 0, max_channels=64)
+    try:
+        rng = np.random.default_rng(coll * 1000 + nt)
+        for dtype, count, soff, doff, nc in [(1, 25 << 19, 0, 0, 8), (0, 300003, 0, 0, 3), (1, 4099, 1, 1, 2),
+                                             (2, 100001, 1, 3, 64), (3, 7, 0, 0, 1), (1, 1 << 20, 0, 5, 17)]:
+            from tests.oracle_ref import random_input
+            x = random_input(dtype, count, rng)
+            want = oracle_collective(coll, 0, dtype, 0, [x])[0]
+            esz = x.itemsize
+            sbase = torch.zeros((count + soff + 8) * esz, dtype=torch.uint8, device="cuda")
+            src = sbase[soff * esz:(soff + count) * esz]
+            src.copy_(torch.from_numpy(x.view(np.uint8)).cuda())
+            dbase = torch.full(((count + doff + 64) * esz,), 0x5A, dtype=torch.uint8, device="cuda")
+            dst = dbase[doff * esz:(doff + count) * esz]
+            dst.fill_(0xAB)
+            comm.launch(coll, C.CollConfig(C.TREE, C.SIMPLE, nc, nt, 2 << 20), dtype, count, src.data_ptr(),
+                        dst.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            comm.check()
+            assert dst.cpu().numpy().tobytes() == want.view(np.uint8).tobytes()
+            g = dbase.cpu().numpy()
+            assert (g[:doff * esz] == 0x5A).all() and (g[(doff + count) * esz:] == 0x5A).all()
+        # in place: no launch, data untouched
+        buf = torch.arange(1000, dtype=torch.int32, device="cuda")
+        comm.launch(coll, C.CollConfig(C.RING, C.SIMPLE, 4, nt, 1 << 20), C.I32, 1000, buf.data_ptr(),
+                    buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(buf, torch.arange(1000, dtype=torch.int32, device="cuda"))
+    finally:
+        comm.close()
+
+
+def test_launches_on_one_comm_keep_issue_order_across_streams(vcomms):
+    """Two collectives on one communicator issued on two streams: the second
+    waits for the first (they share step counters), both bit-exact."""
+    import torch
+    from paper_2602_20656_b200 import coll as C
+    vc = vcomms[4]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs, wants = [], []
+    for i, st in enumerate((s1, s2, s1, s2)):
+        c = dict(coll=C.ALL_REDUCE, algo=C.RING, proto=i % 3, n=4, dtype=0, op=0, nc=4, nt=256, chunk=65536,
+                 count=200003, seed=40 + i)
+        sends = coll_cases.inputs(c)
+        wants.append(oracle_collective(C.ALL_REDUCE, C.RING, 0, 0, sends)[0])
+        dev = [torch.from_numpy(s).cuda() for s in sends]
+        torch.cuda.synchronize()
+        out = [torch.empty_like(d) for d in dev]
+        vc.launch(C.ALL_REDUCE, C.CollConfig(C.RING, i % 3, 4, 256, 65536), 0, 200003,
+                  [t.data_ptr() for t in dev], [t.data_ptr() for t in out], st.cuda_stream, 0)
+        outs.append((dev, out))
+    torch.cuda.synchronize()
+    vc.check()
+    for (dev, out), want in zip(outs, wants):
+        assert out[0].cpu().numpy().tobytes() == want.tobytes()

@@ -25,15 +25,23 @@ def _gpus():
         return 0
 
 
-@pytest.mark.parametrize("nvls", [0, 1])
+@pytest.mark.parametrize("variant", ["p2p", "nvls", "nvls-deep", "nvls-a2a-tma"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_real_multigpu_parity(world, nvls):
-    """nvls=1: buffers in a multicast region, so TREE AllReduce runs inside
+def test_real_multigpu_parity(world, variant):
+    """nvls: buffers in a multicast region, so TREE AllReduce runs inside
     the NVSwitch (int32 and movement bit-exact; fp sums within the stated
-    tolerance, since the switch accumulates in fp32 in its own order)."""
+    bound of the fp64 exact sum, since the switch accumulates in fp32 in its
+    own order). nvls = the co-resident kernels (default), nvls-deep = the
+    deep-unroll ones (coresident = 0), nvls-a2a-tma = the TMA AllToAll."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, LAGOM_NVLS="1") if nvls else dict(os.environ)
+    env = dict(os.environ)
+    if variant != "p2p":
+        env["LAGOM_NVLS"] = "1"
+    if variant == "nvls-deep":
+        env["LAGOM_CORESIDENT"] = "0"
+    if variant == "nvls-a2a-tma":
+        env["LAGOM_A2A_TMA"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]
@@ -54,5 +62,22 @@ def test_real_multigpu_parity_one_hop_allgather_reducescatter(world):
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_real_multigpu_parity_bench_sizes(world):
+    """The bench's own collectives at BASELINE sizes on real peers with NVLS
+    on (TREE = in-switch AR/AG/RS, one-hop A2A; RING = P2P rings), NC 8/16,
+    NT 512, C 2 MiB: bit-exact, or within the fp64-exact-sum bound for the
+    switch's fp32 sums."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_BENCH_SIZES="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_coll_check.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1800, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

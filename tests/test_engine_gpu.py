@@ -21,7 +21,7 @@ def engine():
     from paper_2602_20656_b200 import dags
     dag = dags.gpt2_dp(1, layers=2)
     eng = L.ReplayEngine(json.dumps(dag), f"lagom_test_{os.getpid()}", 0, 1, 0, repeats=1, warmup=0,
-                         nccl=True, e2e_in_bytes=1 << 20, e2e_out_bytes=4096, reserve_comm_sms=True)
+                         nccl=True, e2e_in_bytes=1 << 20, e2e_out_bytes=4096, sm_partition=1)
     yield eng, dag
     eng.stop()
     eng.close()

@@ -29,7 +29,7 @@ def test_coll_library_exports_every_declared_symbol():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     assert set(C.EXPORTED_SYMBOLS) <= set(syms)
-    assert lib.lagom_coll_abi_version() == 1
+    assert lib.lagom_coll_abi_version() == 2
 
 
 def test_other_libraries_load():

@@ -209,7 +209,7 @@ def main():
 
     def engine(d, tag):
         return L.ReplayEngine(json.dumps(d), f"lagom_cp{tag}_{token}", rank, world, local, repeats=3, warmup=1,
-                              nccl=False, reserve_comm_sms=True, nvls=bool(a.nvls), max_channels=64)
+                              nccl=False, sm_partition=2, nvls=bool(a.nvls), max_channels=64)
     eng = engine(dag, "a")
     if rank != 0:  # serve phase 1 (comm alone), then phase 2 (victim overlapped)
         eng.serve()

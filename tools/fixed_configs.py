@@ -55,7 +55,7 @@ def main():
     dag = dags.with_nc_max(dags.BUILDERS[a.workload](world), 64)
     last = dag["compute_ops"][-1]["id"]
     eng = L.ReplayEngine(json.dumps(dag), f"fx_{token}", rank, world, local, repeats=1, warmup=0, nccl=True,
-                         reserve_comm_sms=bool(a.sm_reserve), max_channels=64, nvls=bool(a.nvls))
+                         sm_partition=int(a.sm_reserve), max_channels=64, nvls=bool(a.nvls))
     if rank != 0:
         eng.serve()
         eng.close()
