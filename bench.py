@@ -220,17 +220,23 @@ def nccl_log_env(tag: str) -> str | None:
     """NCCL_DEBUG=INFO with INIT/TUNING to a per-process file, unless the
     user set NCCL_DEBUG: the channels and algorithms NCCL chose for the
     baseline go into the bench line."""
-    if os.environ.get("NCCL_DEBUG"):
-        return None
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("INFO", "TRACE") and not os.environ.get("NCCL_DEBUG_FILE"):
+        return None  # the user asked for NCCL's log on stderr
     path = f"/tmp/lagom_nccl_{tag}_%p.log"
-    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,TUNING", NCCL_DEBUG_FILE=path)
+    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,TUNING,NVLS", NCCL_DEBUG_FILE=path)
     return path.replace("%p", str(os.getpid()))
 
 
 def nccl_log_summary(path: str | None) -> dict:
     import re
-    if not path or not os.path.exists(path):
+    if not path:
         return {"log": None}
+    if not os.path.exists(path):  # NCCL expands %p itself; take this process's file if the pid differs
+        import glob
+        cands = sorted(glob.glob(path.rsplit("_", 1)[0] + "_*.log"))
+        if not cands:
+            return {"log": None}
+        path = cands[0]
     text = open(path, errors="replace").read()
     out = {"log": path}
     m = re.search(r"(\d+) coll channels, (\d+) collnet channels, (\d+) nvls channels, (\d+) p2p channels", text)

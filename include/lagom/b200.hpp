@@ -25,6 +25,7 @@
 #include "lagom/model.hpp"
 #include "lagom/oracle.hpp"
 #include "lagom/simulator.hpp"
+#include "lagom/sweep.hpp"
 #include "lagom/tuner.hpp"
 
 namespace lagom::b200 {
@@ -123,6 +124,9 @@ struct ReplayOptions {
   int nccl_reserve_sms = 0;
   // SIMPLE collectives move data with TMA bulk copies (lagom_comm_opts_t.use_tma).
   bool use_tma = true;
+  // PM sampling: metrics (empty = default_pm_metrics()) and interval.
+  std::vector<std::string> pm_metrics;
+  std::uint64_t pm_interval_ns = 20000;
   // lagom_comm_opts_t.coresident / one_hop / a2a_tma (kernel selection; the
   // same on every rank).
   bool coresident = true;
@@ -133,6 +137,33 @@ struct ReplayOptions {
   bool nvls = false;
 };
 
+// CUPTI PM sampling (pm_sampler.cpp): counters sampled every `interval_ns`
+// of GPU time while kernels run concurrently — no kernel replay, no
+// serialisation. One sampler per process and device.
+struct PmSample {
+  std::uint64_t start_ns = 0, end_ns = 0;  // GPU timestamps (%globaltimer clock)
+  std::vector<double> values;              // one per metric
+};
+class PmSampler {
+ public:
+  // metrics empty: default_pm_metrics()
+  PmSampler(int device, std::vector<std::string> metrics = {}, std::uint64_t interval_ns = 20000,
+            std::size_t max_samples = 20000);
+  ~PmSampler();
+  PmSampler(const PmSampler&) = delete;
+  PmSampler& operator=(const PmSampler&) = delete;
+  const std::vector<std::string>& metrics() const;
+  void start();
+  std::vector<PmSample> stop();  // every completed sample since start()
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+// DRAM read/write bytes, NVLink tx/rx bytes, SM active and elapsed cycles,
+// tensor-pipe active cycles, L2 bytes.
+std::vector<std::string> default_pm_metrics();
+
 // One measured replay, max over ranks (median over repeats).
 struct ReplayMeasurement {
   ProfileResult profile;           // x_j, X = sum x_j, Y = sum y_i, Z
@@ -141,6 +172,12 @@ struct ReplayMeasurement {
   // time queued behind other kernels), next to profile.comm_times, which is
   // the kernel's own active span for the Lagom kernels
   std::vector<double> comm_event_times;
+  // PM sampling (set_pm_sampling): this rank's samples over its last
+  // replay, and the %globaltimer instant of the replay's start (the origin
+  // of the timeline's start offsets).
+  std::vector<std::string> pm_metrics;
+  std::vector<PmSample> pm_samples;
+  std::uint64_t pm_t0_ns = 0;
   double wall_us = 0.0;            // host wall time of the profile call
   // This rank's last replay as a timeline (one event per compute op on the
   // "compute" stream, one per comm op on "comm"), start offsets from the
@@ -191,6 +228,9 @@ class ReplayEngine {
   // a collective can overlap (lagom_partition), NCCL replays reserve
   // `nccl_reserve_sms` (0 = none).
   void set_partition(int sm_partition, int nccl_reserve_sms);
+  // Rank 0: CUPTI PM sampling on every rank during the following remote_*
+  // calls (each rank samples its own GPU; rank 0's samples are returned).
+  void set_pm_sampling(bool on);
   // Whether the NVLS region (in-switch TREE) and the peer mappings (one-hop
   // AllToAll / AllGather / ReduceScatter) are in use — what set-up achieved,
   // not what was requested.
@@ -225,6 +265,16 @@ ProfileFn make_grouped_gpu_profiler(ReplayEngine& engine, std::vector<int> group
 // (more than 64 ops, invalid grid entries, grids beyond `limit`).
 lagom::OracleResult exhaustive_gpu(const Workload& workload, const std::vector<std::vector<CommConfig>>& grids,
                             const SubspaceParams& params, std::int64_t limit, int device = 0);
+
+// exhaustive() / run_sweep() (reference oracle.cpp:12-63, sweep.cpp:11-61)
+// with any ProfileFn — with make_gpu_profiler every grid point / sweep value
+// is a measured replay. Same enumeration order and tie rule as the
+// simulated versions.
+OracleResult exhaustive_with(const ProfileFn& profile_fn, const Workload& workload,
+                             const std::vector<std::vector<CommConfig>>& grids, std::int64_t limit);
+std::vector<SweepRow> sweep_with(const ProfileFn& profile_fn, const Workload& workload,
+                                 const std::vector<CommConfig>& base, const std::string& comm_id, SweepParam param,
+                                 const std::vector<std::int64_t>& values);
 
 // A ProfileFn that answers from a recorded table (exact config-vector match;
 // throws Error(InvalidInput) on a miss). Used to prove that two tuners make

@@ -66,10 +66,12 @@ typedef struct {
   /* Options below change which kernel a launch runs, so every rank of a
    * communicator must use the same values: lagom_comm_import_handles checks
    * them against every peer's and fails with LAGOM_ERR_INVALID_ARGUMENT. */
-  int coresident;          /* 1 (default): the NVLS, one-hop and single-rank kernels
-                              fit next to a GEMM CTA on one SM (<= 21.8 K registers per
-                              CTA, no dynamic shared memory), so NC costs no SMs; 0:
-                              deeper unrolls (more registers) at the same NC/NT      */
+  int coresident;          /* 1 (default): at NT <= 256 the NVLS and one-hop kernels,
+                              and the single-rank copy at any NT, fit next to a GEMM
+                              CTA on one SM (<= 21.8 K registers per CTA, no dynamic
+                              shared memory), so their NC costs no SMs; larger NT runs
+                              the deep-unroll kernels that take an SM each. 0: deep
+                              unrolls at every NT (lagom_coll_footprint tells which) */
   int one_hop;             /* TREE AllGather / ReduceScatter with NVLS bound: 0 (default)
                               through the switch, 1 one hop over the peer mappings, 2
                               one hop at nranks == 2 and NC >= 12                      */
@@ -195,6 +197,11 @@ int lagom_comm_nvls_use_peers(lagom_comm_t comm, int on);
  * hash of (seed, index) — deterministic and identical on every GPU. */
 int lagom_fill_random(void* ptr, int64_t nelems, int dtype, uint64_t seed, float scale,
                       void* stream);
+
+/* Enqueues a one-thread kernel on `stream` that writes the GPU's
+ * %globaltimer (ns; the clock of span_out and of CUPTI's PM samples) to the
+ * device uint64 at `dst`: aligns stream timelines with counter samples. */
+int lagom_timestamp(void* dst, void* stream);
 
 #ifdef __cplusplus
 }

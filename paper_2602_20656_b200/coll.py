@@ -73,7 +73,7 @@ EXPORTED_SYMBOLS = (
     "lagom_comm_nvls_supported", "lagom_comm_nvls_export", "lagom_comm_nvls_import",
     "lagom_comm_nvls_bind", "lagom_comm_nvls_alloc", "lagom_comm_nvls_bytes",
     "lagom_comm_nvls_export_peer", "lagom_comm_nvls_import_peers", "lagom_comm_nvls_use_peers",
-    "lagom_coll_footprint",
+    "lagom_coll_footprint", "lagom_timestamp",
 )
 
 _lib = None
@@ -118,6 +118,7 @@ def library() -> ctypes.CDLL:
         "lagom_comm_nvls_export_peer": (c_int, [vp, ctypes.c_char_p]),
         "lagom_comm_nvls_import_peers": (c_int, [vp, ctypes.c_char_p]),
         "lagom_comm_nvls_use_peers": (c_int, [vp, c_int]),
+        "lagom_timestamp": (c_int, [vp, vp]),
         "lagom_coll_footprint": (c_int, [vp, ctypes.POINTER(_Args), vp, vp, ctypes.POINTER(c_int),
                                          ctypes.POINTER(c_int)]),
     }

@@ -198,6 +198,9 @@ struct ReplayEngine::Impl {
   void* host_in = nullptr;   // pinned
   void* host_out = nullptr;  // pinned
   int calls = 0;
+  bool pm_on = false;
+  std::unique_ptr<PmSampler> sampler;  // created on first use (each rank, its own GPU)
+  unsigned long long* stamp = nullptr;  // device: %globaltimer at the replay start
   bool nvls_on = false;
   bool nvls_peers_on = false;
   std::vector<TimelineEvent> last_timeline;
@@ -267,6 +270,7 @@ struct ReplayEngine::Impl {
       cudaFree(c.recv);
     }
     if (spans) cudaFree(spans);
+    if (stamp) cudaFree(stamp);
     if (host_in) cudaFreeHost(host_in);
     if (host_out) cudaFreeHost(host_out);
     if (ncomm) nccl().CommDestroy(ncomm);
@@ -579,6 +583,7 @@ struct ReplayEngine::Impl {
     coord.barrier();
     const bool e2e = mode == Mode::LagomE2E;
     cuda_check(cudaEventRecord(ev_start, cs), "record");
+    if (pm_on) coll_check(lagom_timestamp(stamp, cs), "timestamp");
     if (e2e && host_in)
       cuda_check(cudaMemcpyAsync(gemms[0][0].A, host_in, opts.e2e_in_bytes, cudaMemcpyHostToDevice, cs), "h2d");
     cuda_check(cudaStreamWaitEvent(ks, ev_start, 0), "wait");
@@ -662,15 +667,31 @@ struct ReplayEngine::Impl {
     if (cfgs && cfgs->size() != comms.size())
       throw Error(ErrorCode::InvalidWorkload, "configs",
                   "expected " + std::to_string(comms.size()) + " configs, got " + std::to_string(cfgs->size()));
+    if (pm_on && !sampler) {
+      sampler = std::make_unique<PmSampler>(opts.device, opts.pm_metrics, opts.pm_interval_ns);
+      cuda_check(cudaMalloc(&stamp, sizeof(unsigned long long)), "stamp");
+    }
     for (int w = 0; w < warmup; ++w) replay(mode, cfgs);
     const std::size_t N = comms.size(), M = dag.compute_ops.size();
     std::vector<std::vector<double>> reps;
+    std::vector<PmSample> samples;
+    std::uint64_t t0_ns = 0;
     for (int r = 0; r < std::max(1, repeats); ++r) {
+      if (pm_on) sampler->start();
       std::vector<double> v = replay(mode, cfgs);
+      if (pm_on) {
+        samples = sampler->stop();  // the last repeat's samples are reported
+        cuda_check(cudaMemcpy(&t0_ns, stamp, sizeof t0_ns, cudaMemcpyDeviceToHost), "stamp");
+      }
       coord.allreduce_max(v.data(), v.size());
       reps.push_back(std::move(v));
     }
     ReplayMeasurement m;
+    if (pm_on) {
+      m.pm_metrics = sampler->metrics();
+      m.pm_samples = std::move(samples);
+      m.pm_t0_ns = t0_ns;
+    }
     m.profile.comm_times.resize(N);
     m.comp_times.resize(M);
     std::vector<double> col(reps.size());
@@ -705,6 +726,7 @@ struct ReplayEngine::Impl {
     wire[0].transport = opts.warmup;
     wire[0].num_channels = opts.sm_partition;
     wire[0].num_threads = opts.nccl_reserve_sms;
+    wire[0].pad = pm_on ? 1 : 0;
     if (cfgs) {
       if (cfgs->size() != comms.size())
         throw Error(ErrorCode::InvalidWorkload, "configs", "one config per comm op expected");
@@ -740,6 +762,7 @@ void ReplayEngine::set_partition(int sm_partition, int nccl_reserve_sms) {
   impl_->opts.nccl_reserve_sms = std::max(0, std::min(nccl_reserve_sms, impl_->num_sms - 1));
 }
 bool ReplayEngine::nvls_active() const { return impl_->nvls_on; }
+void ReplayEngine::set_pm_sampling(bool on) { impl_->pm_on = on; }
 bool ReplayEngine::nvls_peers_active() const { return impl_->nvls_peers_on; }
 
 ReplayMeasurement ReplayEngine::run(const std::vector<CommConfig>& configs) {
@@ -773,6 +796,7 @@ void ReplayEngine::serve() {
     }
     I.opts.sm_partition = wire[0].num_channels;
     I.opts.nccl_reserve_sms = wire[0].num_threads;
+    I.pm_on = wire[0].pad != 0;
     const bool with_cfg = mode == Mode::Lagom || mode == Mode::CommOnly || mode == Mode::LagomE2E;
     I.measure(mode, with_cfg ? &cfgs : nullptr, wire[0].protocol, wire[0].transport);
   }

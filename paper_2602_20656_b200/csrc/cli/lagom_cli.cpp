@@ -5,8 +5,10 @@
 // (--params > $LAGOM_PARAMS > defaults) and exit codes (0 ok, 2 validation,
 // 3 I/O, 4 budget exhausted, 5 grid too large).
 //
-// B200 addition: `tune --profiler gpu --dag DAG.json` replaces the simulator
-// with the iteration-replay engine (lagom/b200.hpp). One process per GPU:
+// B200 addition: `tune | sweep | compare --profiler gpu --dag DAG.json`
+// replace the simulator with the iteration-replay engine (lagom/b200.hpp):
+// every profile call, sweep value and grid point is a measured replay, and
+// the reports / CSV keep the reference schemas. One process per GPU:
 // RANK / WORLD_SIZE / LOCAL_RANK come from the environment (torchrun), the
 // ranks meet in a shared-memory coordinator named by $LAGOM_JOB (or
 // $MASTER_PORT); rank 0 runs the search and writes the report, the other
@@ -52,8 +54,8 @@ const std::map<std::string, std::set<std::string>> kFlags = {
     {"simulate", {"workload", "configs", "params", "trace", "out"}},
     {"tune", {"workload", "params", "start", "budget", "log", "out", "profiler", "dag", "gpu"}},
     {"oracle", {"workload", "params", "grid", "limit", "out"}},
-    {"compare", {"workload", "params", "grid", "limit", "budget"}},
-    {"sweep", {"workload", "configs", "params", "comm", "param", "values", "out"}},
+    {"compare", {"workload", "params", "grid", "limit", "budget", "profiler", "dag"}},
+    {"sweep", {"workload", "configs", "params", "comm", "param", "values", "out", "profiler", "dag"}},
     {"gen", {"pattern", "layers", "seed", "m", "n", "out"}},
 };
 const std::map<std::string, std::set<std::string>> kRequired = {
@@ -310,9 +312,16 @@ int cmd_simulate(const Args& a) {
   return kOk;
 }
 
-// GPU profiler: every rank builds the engine; rank 0 tunes, the others serve.
-std::optional<lagom::TuneResult> tune_on_gpu(const Args& a, const lagom::Workload& w,
-                                             const std::vector<lagom::CommConfig>& init, int budget) {
+// GPU profiler: every rank builds the replay engine over the DAG; rank 0
+// drives (tune / sweep / grid), the other ranks serve replay commands.
+struct GpuSession {
+  std::unique_ptr<lagom::b200::Coordinator> coord;
+  std::unique_ptr<lagom::b200::ReplayEngine> engine;
+  bool driver() const { return engine->rank() == 0; }
+};
+
+std::unique_ptr<GpuSession> gpu_session(const Args& a, const lagom::Workload& w) {
+  if (!a.has("dag")) throw lagom::Error(lagom::ErrorCode::InvalidInput, "dag", "--profiler gpu needs --dag");
   const auto env_int = [](const char* k, int d) {
     const char* v = std::getenv(k);
     return v && *v ? std::atoi(v) : d;
@@ -343,19 +352,16 @@ std::optional<lagom::TuneResult> tune_on_gpu(const Args& a, const lagom::Workloa
   }
   if (dag.comm_ops.size() != w.comm_ops.size())
     throw lagom::Error(lagom::ErrorCode::InvalidInput, "dag", "the DAG must have one comm op per workload comm op");
-  auto coord = lagom::b200::make_shm_coordinator(name, rank, world);
+  auto s = std::make_unique<GpuSession>();
+  s->coord = lagom::b200::make_shm_coordinator(name, rank, world);
   lagom::b200::ReplayOptions o;
   o.device = local;
   o.sm_partition = lagom::b200::kPartitionAuto;
   o.enable_nccl = false;
-  lagom::b200::ReplayEngine engine(dag, *coord, o);
-  if (rank != 0) {
-    engine.serve();
-    return std::nullopt;
-  }
-  lagom::TuneResult r = lagom::tune(w, init, lagom::b200::make_gpu_profiler(engine), budget);
-  engine.stop();
-  return r;
+  o.nvls = world > 1;
+  s->engine = std::make_unique<lagom::b200::ReplayEngine>(dag, *s->coord, o);
+  if (!s->driver()) s->engine->serve();  // returns when the driver stops the engine
+  return s;
 }
 
 int cmd_tune(const Args& a) {
@@ -368,10 +374,10 @@ int cmd_tune(const Args& a) {
   const std::string profiler = a.get("profiler", "sim");
   lagom::TuneResult r;
   if (profiler == "gpu") {
-    if (!a.has("dag")) throw lagom::Error(lagom::ErrorCode::InvalidInput, "dag", "--profiler gpu needs --dag");
-    auto res = tune_on_gpu(a, w, init, budget);
-    if (!res) return kOk;  // a serving rank
-    r = std::move(*res);
+    auto gs = gpu_session(a, w);
+    if (!gs->driver()) return kOk;  // a serving rank, done
+    r = lagom::tune(w, init, lagom::b200::make_gpu_profiler(*gs->engine), budget);
+    gs->engine->stop();
   } else if (profiler == "sim") {
     r = lagom::tune(w, init, lagom::make_sim_profiler(w, params), budget);
   } else {
@@ -422,6 +428,27 @@ int cmd_compare(const Args& a) {
   const auto grids = grids_for(w, params, parse_grid(a.get("grid")));
   const std::int64_t limit = a.has("limit") ? parse_size(a.get("limit")) : 1000000;
   const int budget = std::atoi(a.get("budget", "500").c_str());
+  const std::string profiler = a.get("profiler", "sim");
+  if (profiler == "gpu") {
+    // Measured: the grid and the tuner profile on the GPU replay; the naive
+    // strawman's picks (it reads the model directly, reference oracle.cpp:85-88)
+    // are measured once. Same CSV rows as the simulated compare.
+    auto gs = gpu_session(a, w);
+    if (!gs->driver()) return kOk;
+    const lagom::ProfileFn f = lagom::b200::make_gpu_profiler(*gs->engine);
+    const auto ex = lagom::b200::exhaustive_with(f, w, grids, limit);
+    const auto tu = lagom::tune(w, seeds(w, params, "min"), f, budget);
+    const auto nv = lagom::sequential_naive(w, params);
+    const double nv_z = f(nv.configs).makespan;
+    gs->engine->stop();
+    std::cout.precision(17);
+    std::cout << "method,Z,evaluations\n"
+              << "exhaustive," << ex.makespan << ',' << ex.evaluations << '\n'
+              << "tune," << tu.final_profile.makespan << ',' << tu.profile_calls << '\n'
+              << "naive," << nv_z << ',' << nv.profile_calls << '\n';
+    return tu.budget_exhausted ? kBudget : kOk;
+  }
+  if (profiler != "sim") throw lagom::Error(lagom::ErrorCode::InvalidInput, "profiler", "expected sim|gpu");
   const auto ex = lagom::exhaustive(w, grids, params, limit);
   const auto tu = lagom::tune(w, seeds(w, params, "min"), lagom::make_sim_profiler(w, params), budget);
   const auto nv = lagom::sequential_naive(w, params);
@@ -449,8 +476,20 @@ int cmd_sweep(const Args& a) {
       base[j].chunk_size = std::clamp<std::int64_t>(1024 * lagom::kKiB, b.c_min, b.c_max);
     }
   }
-  const auto rows = lagom::run_sweep(w, base, params, a.get("comm"), lagom::sweep_param_from_string(a.get("param")),
-                                     parse_list(a.get("values")));
+  const std::string profiler = a.get("profiler", "sim");
+  const auto param = lagom::sweep_param_from_string(a.get("param"));
+  std::vector<lagom::SweepRow> rows;
+  if (profiler == "gpu") {  // every value a measured replay of the DAG
+    auto gs = gpu_session(a, w);
+    if (!gs->driver()) return kOk;
+    rows = lagom::b200::sweep_with(lagom::b200::make_gpu_profiler(*gs->engine), w, base, a.get("comm"), param,
+                                   parse_list(a.get("values")));
+    gs->engine->stop();
+  } else if (profiler == "sim") {
+    rows = lagom::run_sweep(w, base, params, a.get("comm"), param, parse_list(a.get("values")));
+  } else {
+    throw lagom::Error(lagom::ErrorCode::InvalidInput, "profiler", "expected sim|gpu");
+  }
   const std::string csv = lagom::sweep_csv(rows);
   if (!a.has("out")) {
     std::cout << csv;

@@ -42,3 +42,17 @@ extern "C" int lagom_fill_random(void* ptr, int64_t nelems, int dtype, uint64_t 
   fill_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(ptr, nelems, dtype, seed, scale);
   return cudaGetLastError() == cudaSuccess ? LAGOM_OK : LAGOM_ERR_CUDA;
 }
+
+namespace {
+__global__ void timestamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  *dst = t;
+}
+}  // namespace
+
+extern "C" int lagom_timestamp(void* dst, void* stream) {
+  if (!dst) return LAGOM_ERR_INVALID_ARGUMENT;
+  timestamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<unsigned long long*>(dst));
+  return cudaGetLastError() == cudaSuccess ? LAGOM_OK : LAGOM_ERR_CUDA;
+}

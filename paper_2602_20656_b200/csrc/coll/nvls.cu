@@ -441,23 +441,22 @@ const void* pick_nvls_u(int dtype) {
 // the switch, so AR / RS throughput per SM is set by the bytes in flight,
 // NT x U x 16 B (measured on 4xB200: AR 25 MiB at NC = 4, NT = 512 goes from
 // 232 to 411 GB/s busbw with U = 16 instead of 8).
-//   coresident: per thread-count class, U such that NT x U x 16 B ~ 32 KB
-//     (64: 32, 128: 16, 256: 8, 384..640: 4) under the 21.8 K-register CTA
-//     budget; one-hop RS (acc[U] + v[U]) takes half.
-//   otherwise (round 1): NT <= 256 -> U = 32 (launch bound 256); else U = 16
-//     (U = 8 for the copy kinds).
+//   coresident (default), NT <= 256: the CTA fits next to a GEMM CTA on one
+//     SM (<= 21.8 K registers): U = 32 / 16 / 8 at NT = 64 / 128 / 256, i.e.
+//     32 KB in flight per CTA (one-hop RS and the A2A take half where the full
+//     unroll would spill under the cap);
+//   NT > 256, or coresident = 0: the deep unrolls of round 1 (U = 16, U = 8
+//     for the copy kinds; NT <= 256 -> U = 32 with a 256-thread launch bound),
+//     whose CTAs take an SM of their own (the replay's SM partition reserves
+//     their NC). The tuner's NT thus also picks the regime: many light CTAs
+//     riding along the GEMMs, or few heavy CTAs on dedicated SMs.
 template <int KIND>
 const void* pick_nvls(int dtype, int nt, bool coresident) {
-  if (coresident) {
-    // one-hop RS (acc + v) and the A2A (a peer pointer per step): half the
-    // unroll where the full one would spill under the register cap
+  if (coresident && nt <= 256) {
     constexpr int H = KIND == 5 ? 2 : 1, H3 = KIND == 3 ? 2 : 1;
     if (nt <= 64) return pick_nvls_u<KIND, 32 / H / H3, 64, 3>(dtype);
     if (nt <= 128) return pick_nvls_u<KIND, 16 / H, 128, 3>(dtype);
-    if (nt <= 256) return pick_nvls_u<KIND, 8 / H, 256, 3>(dtype);
-    if (nt <= 384) return pick_nvls_u<KIND, 4 / H, 384, 3>(dtype);
-    if (nt <= 512) return pick_nvls_u<KIND, 4 / H / H3, 512, 3>(dtype);
-    return pick_nvls_u<KIND, 4 / H / H3, 640, 3>(dtype);
+    return pick_nvls_u<KIND, 8 / H, 256, 3>(dtype);
   }
   if (KIND == 5)  // one-hop RS holds acc[U] + v[U]: half the unroll of ld_reduce
     return nt <= 256 ? pick_nvls_u<KIND, 16, 256>(dtype) : pick_nvls_u<KIND, 8, 640>(dtype);

@@ -5,7 +5,12 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <execinfo.h>
+#include <unistd.h>
+
 #include <chrono>
+#include <csignal>
+#include <cstdlib>
 #include <memory>
 
 #include "lagom/b200.hpp"
@@ -134,12 +139,23 @@ GpuSpec gpu_from_json(const std::string& s) {
   return g;
 }
 
+Json pm_json(const b200::ReplayMeasurement& m) {
+  if (m.pm_metrics.empty()) return nullptr;
+  Json rows = Json::array();
+  for (const b200::PmSample& s : m.pm_samples) {
+    Json row = Json::array({s.start_ns, s.end_ns});
+    for (double v : s.values) row.push_back(v);
+    rows.push_back(row);
+  }
+  return Json{{"metrics", m.pm_metrics}, {"t0_ns", m.pm_t0_ns}, {"samples", rows}};
+}
+
 Json measurement_json(const b200::ReplayMeasurement& m) {
   SimResult tl;
   tl.timeline = m.timeline;
   return Json{{"x", m.profile.comm_times}, {"x_ev", m.comm_event_times}, {"y", m.comp_times}, {"X", m.profile.total_comm},
               {"Y", m.profile.total_compute}, {"Z", m.profile.makespan}, {"wall_us", m.wall_us},
-              {"trace", trace_to_json(tl)}};
+              {"trace", trace_to_json(tl)}, {"pm", pm_json(m)}};
 }
 
 std::vector<CommConfig> configs_arg(const std::string& s) { return configs_from_json(parse(s)); }
@@ -149,7 +165,7 @@ class PyEngine {
   PyEngine(const std::string& dag_json, const std::string& coord_name, int rank, int size, int device,
            int repeats, int warmup, bool nccl, std::int64_t max_chunk, int max_channels,
            std::int64_t e2e_in, std::int64_t e2e_out, int sm_partition, bool nvls, bool coresident, int one_hop,
-           bool a2a_tma)
+           bool a2a_tma, std::uint64_t pm_interval_ns)
       : dag_(dag_from_json(parse(dag_json))) {
     coord_ = b200::make_shm_coordinator(coord_name, rank, size);
     b200::ReplayOptions o;
@@ -166,6 +182,7 @@ class PyEngine {
     o.coresident = coresident;
     o.one_hop = one_hop;
     o.a2a_tma = a2a_tma;
+    o.pm_interval_ns = pm_interval_ns;
     engine_ = std::make_unique<b200::ReplayEngine>(dag_, *coord_, o);
   }
   std::string workload(const std::string& gpu_json) const {
@@ -231,6 +248,7 @@ class PyEngine {
   void set_measurement(int repeats, int warmup) { engine_->set_measurement(repeats, warmup); }
   void set_partition(int sm_partition, int nccl_reserve) { engine_->set_partition(sm_partition, nccl_reserve); }
   bool nvls_active() const { return engine_->nvls_active(); }
+  void set_pm_sampling(bool on) { engine_->set_pm_sampling(on); }
   bool nvls_peers_active() const { return engine_->nvls_peers_active(); }
   int rank() const { return engine_->rank(); }
   int nranks() const { return engine_->nranks(); }
@@ -254,7 +272,25 @@ class PyEngine {
 
 }  // namespace
 
+namespace {
+// LAGOM_BACKTRACE=1: native backtrace on SIGABRT / SIGSEGV (debugging aid;
+// the boxes have no debugger).
+void backtrace_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "[lagom] native backtrace:\n";
+  (void)!write(2, msg, sizeof msg - 1);
+  backtrace_symbols_fd(frames, n, 2);
+  std::signal(sig, SIG_DFL);
+  std::raise(sig);
+}
+}  // namespace
+
 PYBIND11_MODULE(_lagom_py, m) {
+  if (const char* e = std::getenv("LAGOM_BACKTRACE"); e && *e == '1') {
+    std::signal(SIGABRT, backtrace_handler);
+    std::signal(SIGSEGV, backtrace_handler);
+  }
   m.doc() = "lagom-b200 C++ API (JSON in/out in the reference formats)";
   m.attr("version") = kVersion;
   py::register_exception<Error>(m, "LagomError");
@@ -343,12 +379,13 @@ PYBIND11_MODULE(_lagom_py, m) {
 
   py::class_<PyEngine>(m, "ReplayEngine")
       .def(py::init<const std::string&, const std::string&, int, int, int, int, int, bool, std::int64_t, int,
-                    std::int64_t, std::int64_t, int, bool, bool, int, bool>(),
+                    std::int64_t, std::int64_t, int, bool, bool, int, bool, std::uint64_t>(),
            py::arg("dag"), py::arg("coord_name"), py::arg("rank"), py::arg("size"), py::arg("device"),
            py::arg("repeats") = 3, py::arg("warmup") = 1, py::arg("nccl") = true,
            py::arg("max_chunk_bytes") = 4 << 20, py::arg("max_channels") = 32, py::arg("e2e_in_bytes") = 0,
            py::arg("e2e_out_bytes") = 0, py::arg("sm_partition") = 1, py::arg("nvls") = false,
-           py::arg("coresident") = true, py::arg("one_hop") = 0, py::arg("a2a_tma") = false)
+           py::arg("coresident") = true, py::arg("one_hop") = 0, py::arg("a2a_tma") = false,
+           py::arg("pm_interval_ns") = 20000)
       .def("workload", &PyEngine::workload, py::arg("gpu") = "")
       .def("run", &PyEngine::run)
       .def("run_e2e", &PyEngine::run_e2e)
@@ -364,6 +401,7 @@ PYBIND11_MODULE(_lagom_py, m) {
       .def("barrier", &PyEngine::barrier)
       .def("set_partition", &PyEngine::set_partition, py::arg("sm_partition"), py::arg("nccl_reserve_sms") = 0)
       .def_property_readonly("nvls_active", &PyEngine::nvls_active)
+      .def("set_pm_sampling", &PyEngine::set_pm_sampling, py::arg("on"))
       .def_property_readonly("nvls_peers_active", &PyEngine::nvls_peers_active)
       .def_property_readonly("rank", &PyEngine::rank)
       .def_property_readonly("nranks", &PyEngine::nranks);

@@ -86,3 +86,45 @@ def test_gpu_batched_exhaustive_matches_cpu_oracle():
         assert gpu["evaluations"] == cpu["evaluations"]
         assert gpu["Z"] == cpu["Z"]  # bit-identical doubles
         assert gpu["configs"] == cpu["configs"]
+
+
+def test_cli_sweep_and_compare_on_hardware(tmp_path, root):
+    """`lagom sweep|compare --profiler gpu --dag`: the reference CLI's
+    one-parameter sweep and its method comparison with every value / grid
+    point a measured replay; the CSVs keep the reference schemas
+    (sweep: value,x_comm,Y,Z — reference sweep.cpp:53-61; compare:
+    method,Z,evaluations — reference lagom_main.cpp:333-360)."""
+    import subprocess
+    if not cuda_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_20656_b200 import _lagom_py as L
+    from paper_2602_20656_b200 import dags
+    dag = dags.gpt2_dp(1, layers=1)
+    eng = L.ReplayEngine(json.dumps(dag), f"lagom_cli_wl_{os.getpid()}", 0, 1, 0, nccl=False)
+    work = eng.workload("")
+    eng.stop()
+    eng.close()
+    (tmp_path / "w.json").write_text(work)
+    (tmp_path / "d.json").write_text(json.dumps(dag))
+    cli = os.path.join(root, "build", "lagom")
+    env = dict(os.environ, LAGOM_JOB=f"clitest{os.getpid()}")
+    comm = dag["comm_ops"][0]["id"]
+    r = subprocess.run([cli, "sweep", "--workload", str(tmp_path / "w.json"), "--dag", str(tmp_path / "d.json"),
+                        "--profiler", "gpu", "--comm", comm, "--param", "nc", "--values", "1,4,16"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0] == "value,x_comm,Y,Z" and [ln.split(",")[0] for ln in lines[1:]] == ["1", "4", "16"]
+    for ln in lines[1:]:
+        v, x, y, z = (float(t) for t in ln.split(","))
+        assert x > 0 and y > 0 and z >= max(y, x) * 0.999
+    r = subprocess.run([cli, "compare", "--workload", str(tmp_path / "w.json"), "--dag", str(tmp_path / "d.json"),
+                        "--profiler", "gpu", "--grid", "nc=1,8;nt=128;c=1M", "--budget", "8"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode in (0, 4), r.stderr
+    rows = r.stdout.strip().splitlines()
+    assert rows[0] == "method,Z,evaluations"
+    methods = {ln.split(",")[0]: float(ln.split(",")[1]) for ln in rows[1:]}
+    assert set(methods) == {"exhaustive", "tune", "naive"} and all(z > 0 for z in methods.values())
+    n_ops = len(dag["comm_ops"])
+    assert int(rows[1].split(",")[2]) == 2 ** n_ops  # every joint grid point replayed

@@ -30,13 +30,30 @@ def test_refit_reproduces_the_bench_params(tmp_path):
     assert set(got["collective_factors"]) == {"ALL_REDUCE", "ALL_GATHER", "REDUCE_SCATTER", "ALL_TO_ALL"}
 
 
-@pytest.mark.parametrize("workload", ["gpt2-1.3b-dp", "llama3-8b-tp-sp"])
-def test_predicted_overlap_time_within_stated_bound(tmp_path, workload):
-    bench = os.path.join(ROOT, "profiles", f"round1_final_n4_{workload}.json")
+ROWS = [(n, w) for n in (4, 2) for w in ("gpt2-1.3b-dp", "llama3-8b-tp-sp", "llama3-70b-fsdp", "mixtral-8x7b-ep")]
+# Stated bound: |predicted Z - measured Z| <= 5 % of measured.
+# Rows the round-1 model misses are pinned at their real errors, not skipped.
+OUT_OF_BOUND = {(4, "llama3-70b-fsdp"), (4, "mixtral-8x7b-ep"), (2, "llama3-70b-fsdp"), (2, "mixtral-8x7b-ep")}
+
+
+@pytest.fixture(scope="module")
+def fit_cache(tmp_path_factory):
+    return str(tmp_path_factory.mktemp("fit") / "fit.json")
+
+
+@pytest.mark.parametrize("n,workload", ROWS, ids=[f"n{n}-{w}" for n, w in ROWS])
+def test_predicted_overlap_time_all_rows(tmp_path, fit_cache, n, workload):
+    """Every (config, N) row of DESIGN.md §6 re-derived from the committed
+    profile and bench files: the prediction is reproduced bit for bit, the
+    relative Z error equals the committed one, and it is inside the stated
+    5 % bound exactly for the rows DESIGN.md says are inside."""
+    bench = os.path.join(ROOT, "profiles", f"round1_final_n{n}_{workload}.json")
     out = tmp_path / "pvm.json"
     subprocess.run([sys.executable, os.path.join(ROOT, "tools", "predict_vs_measured.py"), "--profile", PROFILE,
-                    "--bench", bench, "--out", str(out)], cwd=ROOT, check=True, capture_output=True, timeout=600)
+                    "--bench", bench, "--out", str(out), "--fit-cache", fit_cache], cwd=ROOT, check=True,
+                   capture_output=True, timeout=600)
     got = json.load(open(out))
-    committed = json.load(open(os.path.join(ROOT, "profiles", f"round1_predict_vs_measured_n4_{workload}.json")))
+    committed = json.load(open(os.path.join(ROOT, "profiles", f"round1_predict_vs_measured_n{n}_{workload}.json")))
     assert got["predicted"]["Z"] == pytest.approx(committed["predicted"]["Z"], rel=1e-12)
-    assert abs(got["rel_err"]["Z"]) <= 0.05  # stated bound on Z
+    assert got["rel_err"]["Z"] == pytest.approx(committed["rel_err"]["Z"], rel=1e-9)
+    assert (abs(got["rel_err"]["Z"]) <= 0.05) == ((n, workload) not in OUT_OF_BOUND)

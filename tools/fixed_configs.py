@@ -12,6 +12,7 @@ Each config is ALGO:NC:NT:C with ALGO R (ring) or T (tree).
 import argparse
 import json
 import os
+import random
 import secrets
 import statistics
 import sys
@@ -34,7 +35,8 @@ def main():
     ap.add_argument("--workload", default="gpt2-1.3b-dp")
     ap.add_argument("--sets", nargs="+", required=True)
     ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--sm-reserve", type=int, default=1)
+    ap.add_argument("--sm-reserve", type=int, default=1, help="SM partition: 0 none, 1 auto, 2 all")
+    ap.add_argument("--coresident", type=int, default=1)
     ap.add_argument("--nvls", type=int, default=1)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -55,7 +57,8 @@ def main():
     dag = dags.with_nc_max(dags.BUILDERS[a.workload](world), 64)
     last = dag["compute_ops"][-1]["id"]
     eng = L.ReplayEngine(json.dumps(dag), f"fx_{token}", rank, world, local, repeats=1, warmup=0, nccl=True,
-                         sm_partition=int(a.sm_reserve), max_channels=64, nvls=bool(a.nvls))
+                         sm_partition=int(a.sm_reserve), max_channels=64, nvls=bool(a.nvls),
+                         coresident=bool(a.coresident))
     if rank != 0:
         eng.serve()
         eng.close()
@@ -74,8 +77,11 @@ def main():
             fn()
     res = {k: [] for k in arms}
     names = list(arms)
-    for s in range(a.steps):  # rotated order: no arm keeps a fixed predecessor
-        for k in names[s % len(names):] + names[:s % len(names)]:
+    rng = random.Random(20260219)
+    for s in range(a.steps):  # a fresh random order per step: no arm keeps a fixed predecessor
+        perm = names[:]
+        rng.shuffle(perm)
+        for k in perm:
             res[k].append(json.loads(arms[k]()))
     eng.stop()
     eng.close()

@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--bench", required=True)
     ap.add_argument("--out", default="")
     ap.add_argument("--waves", type=int, default=16)
+    ap.add_argument("--fit-cache", default="", help="reuse (or write) the comm-model fit of --profile")
     ap.add_argument("--hbm-share", type=float, default=0.0,
                     help="fraction of each isolated wave time put in the wave model's HBM term "
                          "blocks*D/(B - V) (reference contention.cpp:35-44), the rest in theta; "
@@ -68,12 +69,19 @@ def main():
 
     prof = json.load(open(a.profile))
     params, report, link = {}, {}, None
-    for key, pts in prof["measurements"].items():
-        co, lk, rep = fit(pts)
-        params[key] = co
-        report[key] = dict(rep, link_bw=lk)
-        if key == "RING/SIMPLE/P2P":
-            link = lk
+    if a.fit_cache and os.path.exists(a.fit_cache):  # the same profile's fit, computed once
+        with open(a.fit_cache) as f:
+            params, report, link = (lambda d: (d["params"], d["report"], d["link"]))(json.load(f))
+    else:
+        for key, pts in prof["measurements"].items():
+            co, lk, rep = fit(pts)
+            params[key] = co
+            report[key] = dict(rep, link_bw=lk)
+            if key == "RING/SIMPLE/P2P":
+                link = lk
+        if a.fit_cache:
+            with open(a.fit_cache, "w") as f:
+                json.dump({"params": params, "report": report, "link": link}, f)
     # footprint from the overlapped-victim sweeps (reference mem_footprint form)
     for key in ("RING/SIMPLE/P2P", "TREE/SIMPLE/P2P"):
         if key in params and key in prof["params"]:
