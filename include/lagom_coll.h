@@ -73,8 +73,10 @@ typedef struct {
                               the deep-unroll kernels that take an SM each. 0: deep
                               unrolls at every NT (lagom_coll_footprint tells which) */
   int one_hop;             /* TREE AllGather / ReduceScatter with NVLS bound: 0 (default)
-                              through the switch, 1 one hop over the peer mappings, 2
-                              one hop at nranks == 2 and NC >= 12                      */
+                              through the switch, 1 one hop over the peer mappings
+                              (AG: peer stores; RS: pushes into the owners' scratch, see
+                              lagom_comm_nvls_scratch), 2 one hop at nranks == 2 (where
+                              the multicast echo caps the switch schedules)           */
   int a2a_tma;             /* one-hop AllToAll through the TMA engine (192 KB smem ring
                               per CTA, cannot share an SM with a GEMM); default 0      */
 } lagom_comm_opts_t;
@@ -187,6 +189,12 @@ int64_t lagom_comm_nvls_bytes(lagom_comm_t comm);
  * lagom_comm_destroy, so peers may import at any time before that. */
 int lagom_comm_nvls_export_peer(lagom_comm_t comm, void* blob /* LAGOM_HANDLE_BYTES */);
 int lagom_comm_nvls_import_peers(lagom_comm_t comm, const void* blobs);
+/* Reserves the push-based one-hop ReduceScatter's scratch in the NVLS region:
+ * nranks slots of slot_bytes (slot q receives rank q's partial of this
+ * rank's block). Same call order on every rank (symmetric offsets, like
+ * lagom_comm_nvls_alloc). Without it (or for blocks larger than a slot) the
+ * one-hop ReduceScatter pulls peers' partials instead of receiving pushes. */
+int lagom_comm_nvls_scratch(lagom_comm_t comm, int64_t slot_bytes);
 /* Switches the one-hop AllToAll on (1) or off (0). Must be agreed on by all
  * ranks (call it with the same value everywhere once every rank imported),
  * since sender and receiver must use the same schedule. */

@@ -73,7 +73,7 @@ EXPORTED_SYMBOLS = (
     "lagom_comm_nvls_supported", "lagom_comm_nvls_export", "lagom_comm_nvls_import",
     "lagom_comm_nvls_bind", "lagom_comm_nvls_alloc", "lagom_comm_nvls_bytes",
     "lagom_comm_nvls_export_peer", "lagom_comm_nvls_import_peers", "lagom_comm_nvls_use_peers",
-    "lagom_coll_footprint", "lagom_timestamp",
+    "lagom_coll_footprint", "lagom_timestamp", "lagom_comm_nvls_scratch",
 )
 
 _lib = None
@@ -119,6 +119,7 @@ def library() -> ctypes.CDLL:
         "lagom_comm_nvls_import_peers": (c_int, [vp, ctypes.c_char_p]),
         "lagom_comm_nvls_use_peers": (c_int, [vp, c_int]),
         "lagom_timestamp": (c_int, [vp, vp]),
+        "lagom_comm_nvls_scratch": (c_int, [vp, c_i64]),
         "lagom_coll_footprint": (c_int, [vp, ctypes.POINTER(_Args), vp, vp, ctypes.POINTER(c_int),
                                          ctypes.POINTER(c_int)]),
     }
@@ -261,6 +262,11 @@ class Communicator:
             return False  # every rank got here: the one-hop schedules stay off everywhere
         _check(lib.lagom_comm_nvls_use_peers(self._h, 1), "nvls")
         return True
+
+    def nvls_scratch(self, slot_bytes: int) -> None:
+        """Reserves the push-based one-hop ReduceScatter's scratch (n slots;
+        same call order on every rank)."""
+        _check(library().lagom_comm_nvls_scratch(self._h, slot_bytes), "nvls")
 
     def nvls_alloc(self, nbytes: int) -> int:
         """Device pointer into the NVLS region (same offset on every rank when

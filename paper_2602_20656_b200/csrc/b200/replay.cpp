@@ -403,7 +403,11 @@ struct ReplayEngine::Impl {
     }
     // NVLS region sized for every comm op's send + recv buffers (4 KiB aligned).
     if (opts.nvls && n > 1 && lagom_comm_nvls_supported(lcomm)) {
-      std::int64_t need = 1 << 20;
+      std::int64_t need = 1 << 20, rs_slot = 0;
+      for (const ReplayCommOp& op : dag.comm_ops)
+        if (op.collective == Collective::ReduceScatter)
+          rs_slot = std::max<std::int64_t>(rs_slot, op.count * elem_bytes(op.dtype));
+      if (opts.one_hop && rs_slot > 0) need += (rs_slot + 4095) / 4096 * 4096 * n + 4096;  // push-RS scratch
       for (const ReplayCommOp& op : dag.comm_ops) {
         const bool in_full = op.collective == Collective::ReduceScatter || op.collective == Collective::AllToAll;
         const bool out_full = op.collective == Collective::AllGather || op.collective == Collective::AllToAll;
@@ -426,6 +430,7 @@ struct ReplayEngine::Impl {
         ok = agree(lagom_comm_nvls_import(lcomm, blob) == LAGOM_OK);
       }
       if (ok) ok = agree(lagom_comm_nvls_bind(lcomm) == LAGOM_OK);
+      if (ok && opts.one_hop && rs_slot > 0) coll_check(lagom_comm_nvls_scratch(lcomm, rs_slot), "nvls scratch");
       nvls_on = ok;
       if (ok) {  // peer mappings: one-hop AllToAll (TREE) into the peers' recv buffers
         unsigned char mine[LAGOM_HANDLE_BYTES];

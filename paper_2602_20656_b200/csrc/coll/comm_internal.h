@@ -31,6 +31,8 @@ struct lagom_comm {
   char* nvls_mc = nullptr;                  // multicast mapping (all ranks)
   int64_t nvls_bytes = 0;
   int64_t nvls_used = 0;
+  char* nvls_scratch = nullptr;             // push-based one-hop RS: n slots of scratch_slot bytes
+  int64_t nvls_scratch_slot = 0;
   bool nvls_ready = false;
   int64_t off_nvbar = 0, off_nvep = 0;      // NVLS barrier flags / epochs in the heap
   int nvls_export_fd = -1;                  // rank 0's exported fd, closed once bound

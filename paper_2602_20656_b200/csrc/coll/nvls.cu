@@ -92,8 +92,11 @@ struct NvlsParams {
   unsigned int* abort_flag;
   uint64_t timeout_ns;
   unsigned long long* span;
-  char* peer_recv[LAGOM_MAX_RANKS];        // one-hop A2A / AG: recv in every rank's region
-  const char* peer_send[LAGOM_MAX_RANKS];  // one-hop RS: send in every rank's region
+  char* peer_recv[LAGOM_MAX_RANKS];        // one-hop A2A / AG: recv in every rank's region;
+                                           // push RS: every rank's scratch slot for me
+  const char* peer_send[LAGOM_MAX_RANKS];  // one-hop RS (pull): send in every rank's region
+  char* scratch;                           // push RS: my scratch (slot q holds rank q's partial)
+  int64_t scratch_slot;                    // bytes per scratch slot
 };
 
 __device__ bool nv_wait(const uint64_t* p, uint64_t v, const NvlsParams& P) {
@@ -252,6 +255,29 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
           if (u0 + j * nt < hi) *reinterpret_cast<uint4*>(out + (u0 + j * nt) * 16) = v[j];
       }
     }
+  } else if constexpr (KIND == 6) {
+    // Push-based one-hop ReduceScatter, phase 1: my partial of every other
+    // rank's block goes straight into that rank's scratch slot for me (one
+    // posted NVLink write per byte, no round trip). Phase 2 runs after the
+    // mid barrier below.
+    for (int k = 1; k < n; ++k) {
+      const int p = (r + k) % n;
+      const uint4* src = reinterpret_cast<const uint4*>(P.send_uc + static_cast<int64_t>(p) * units * 16) + lo;
+      uint4* dst = reinterpret_cast<uint4*>(P.peer_recv[p]) + lo;
+      int64_t left = hi - lo - threadIdx.x;
+      src += threadIdx.x;
+      dst += threadIdx.x;
+      for (; left > (U - 1) * nt; left -= U * nt) {
+        uint4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) v[j] = src[j * nt];
+#pragma unroll
+        for (int j = 0; j < U; ++j) dst[j * nt] = v[j];
+        src += U * nt;
+        dst += U * nt;
+      }
+      for (; left > 0; left -= nt, src += nt, dst += nt) *dst = *src;
+    }
   } else if constexpr (KIND == 5) {
     // One-hop ReduceScatter: pull block r of every rank's send through the
     // peer mappings and combine in the ring order (x_{r+1}, then x_{r+2}, ...,
@@ -344,10 +370,44 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();  // my multimem / peer stores are visible everywhere
-    const bool ok = nv_barrier(P, ch, ep + 1);  // nobody reads results / reuses inputs early
-    if (ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
-    if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+    // AR / AG / RS / A2A: nobody reads results or reuses inputs early. Push
+    // RS: every peer's partial for my block has landed in my scratch (the
+    // next launch's entry barrier keeps peers from overwriting it while I
+    // reduce below).
+    s_ok = nv_barrier(P, ch, ep + 1) ? 1 : 0;
+    if (s_ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
   }
+  if constexpr (KIND == 6) {
+    // Phase 2: reduce my block in the ring order — acc = x_{r+1}, then
+    // x_{r+2}, ..., ending with my own x_r, every combine rounding to the
+    // element type — so the result is bit-identical to the ring schedule
+    // and its oracle. Peers' partials are local now (scratch slot q).
+    __syncthreads();
+    if (s_ok) {
+      using R = lagom_dev::Red<T, LAGOM_SUM>;
+      const char* own = P.send_uc + static_cast<int64_t>(r) * units * 16;
+      auto part = [&](int q) -> const uint4* {
+        return reinterpret_cast<const uint4*>(q == r ? own : P.scratch + static_cast<int64_t>(q) * P.scratch_slot);
+      };
+      uint4* out = reinterpret_cast<uint4*>(P.recv_uc);
+      for (int64_t u = lo + threadIdx.x; u < hi; u += nt * U) {
+        uint4 acc[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u + j * nt < hi) acc[j] = part((r + 1) % n)[u + j * nt];
+        for (int k = 2; k <= n; ++k) {
+          const uint4* x = part((r + k) % n);
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (u + j * nt < hi) acc[j] = lagom_dev::red4<R>(x[u + j * nt], acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u + j * nt < hi) out[u + j * nt] = acc[j];
+      }
+    }
+  }
+  if (threadIdx.x == 0 && P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
 }
 
 // One-hop AllToAll through the TMA engine: thread 0 streams every (peer,
@@ -453,12 +513,12 @@ const void* pick_nvls_u(int dtype) {
 template <int KIND>
 const void* pick_nvls(int dtype, int nt, bool coresident) {
   if (coresident && nt <= 256) {
-    constexpr int H = KIND == 5 ? 2 : 1, H3 = KIND == 3 ? 2 : 1;
+    constexpr int H = (KIND == 5 || KIND == 6) ? 2 : 1, H3 = KIND == 3 ? 2 : 1;
     if (nt <= 64) return pick_nvls_u<KIND, 32 / H / H3, 64, 3>(dtype);
     if (nt <= 128) return pick_nvls_u<KIND, 16 / H, 128, 3>(dtype);
     return pick_nvls_u<KIND, 8 / H, 256, 3>(dtype);
   }
-  if (KIND == 5)  // one-hop RS holds acc[U] + v[U]: half the unroll of ld_reduce
+  if (KIND == 5 || KIND == 6)  // one-hop RS holds acc[U] + v[U]: half the unroll of ld_reduce
     return nt <= 256 ? pick_nvls_u<KIND, 16, 256>(dtype) : pick_nvls_u<KIND, 8, 640>(dtype);
   if (nt <= 256) return pick_nvls_u<KIND, 32, 256>(dtype);
   return (KIND == 1 || KIND == 3 || KIND == 4) ? pick_nvls_u<KIND, 8, 640>(dtype) : pick_nvls_u<KIND, 16, 640>(dtype);
@@ -483,11 +543,12 @@ int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 :
 // busbw from NC = 8 upward, while the one-hop schedules keep scaling with the
 // channels (AllGather on a 4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355
 // vs 278; NC 32: 569 vs 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl).
-// one_hop = 2 follows the config (one hop at n = 2 and NC >= 12; every rank
-// launches the same config, so every rank makes the same choice).
+// one_hop = 2: one hop at n = 2 (every rank has the same n, so every rank
+// makes the same choice).
 bool one_hop(const lagom_comm* c, int nc) {
   const int mode = c->opts.one_hop;
-  return c->nvls_peers_ready && (mode == 1 || (mode == 2 && c->nranks == 2 && nc >= 12));
+  (void)nc;
+  return c->nvls_peers_ready && (mode == 1 || (mode == 2 && c->nranks == 2));
 }
 
 int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,
@@ -496,6 +557,7 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   if (!c->nvls_ready || a->algorithm != LAGOM_TREE || a->redop != LAGOM_SUM || c->virt) return 0;
   const int64_t e = ebytes(a->dtype), n = c->nranks;
   const bool co = c->opts.coresident != 0, hop = one_hop(c, a->num_channels);
+  const bool push_rs = hop && c->nvls_scratch && a->count * ebytes(a->dtype) <= c->nvls_scratch_slot;
   int64_t in_b = 0, out_b = 0;
   const void* k = nullptr;
   switch (a->collective) {
@@ -508,7 +570,10 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
     case LAGOM_REDUCE_SCATTER:
       in_b = a->count * e * n;
       out_b = a->count * e;
-      k = hop ? pick_nvls<5>(a->dtype, a->num_threads, co) : pick_nvls<2>(a->dtype, a->num_threads, co);
+      // one hop: push (partials into the owners' scratch, local reduce) when a
+      // scratch slot fits the block, else pull (peer loads; latency-bound)
+      k = !hop ? pick_nvls<2>(a->dtype, a->num_threads, co)
+          : push_rs ? pick_nvls<6>(a->dtype, a->num_threads, co) : pick_nvls<5>(a->dtype, a->num_threads, co);
       break;
     case LAGOM_ALL_TO_ALL:
       if (!c->nvls_peers_ready) return 0;
@@ -534,7 +599,7 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   // the one-hop RS reads peer_send: both buffers must be in the region too
   const bool a2a = a->collective == LAGOM_ALL_TO_ALL || (a->collective == LAGOM_ALL_GATHER && hop);
   const bool send_mc = a->collective != LAGOM_ALL_GATHER && !a2a, recv_mc = a->collective != LAGOM_REDUCE_SCATTER;
-  const bool need_send = send_mc || (a->collective == LAGOM_REDUCE_SCATTER && hop);
+  const bool need_send = send_mc || (a->collective == LAGOM_REDUCE_SCATTER && hop && !push_rs);
   const bool need_recv = recv_mc || a2a;
   // Buffer placement is per rank: a rank that fell back to P2P here while
   // its peers ran the switch kernel would wait on flags nobody writes, so a
@@ -557,9 +622,15 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   p.recv_mc = recv_mc && !a2a ? c->nvls_mc + (static_cast<char*>(recv) - c->nvls_uc) : nullptr;
   if (a2a)
     for (int q = 0; q < c->nranks; ++q) p.peer_recv[q] = c->nvls_peer[q] + (static_cast<char*>(recv) - c->nvls_uc);
-  if (a->collective == LAGOM_REDUCE_SCATTER && hop)
+  if (a->collective == LAGOM_REDUCE_SCATTER && hop && !push_rs)
     for (int q = 0; q < c->nranks; ++q)
       p.peer_send[q] = c->nvls_peer[q] + (static_cast<const char*>(send) - c->nvls_uc);
+  if (a->collective == LAGOM_REDUCE_SCATTER && push_rs) {
+    const int64_t at = (c->nvls_scratch - c->nvls_uc) + static_cast<int64_t>(c->rank) * c->nvls_scratch_slot;
+    for (int q = 0; q < c->nranks; ++q) p.peer_recv[q] = c->nvls_peer[q] + at;  // my slot in q's scratch
+    p.scratch = c->nvls_scratch;
+    p.scratch_slot = c->nvls_scratch_slot;
+  }
   p.off_nvbar = c->off_nvbar;
   p.off_nvep = c->off_nvep;
   p.abort_flag = c->abort_dev;
@@ -683,6 +754,17 @@ int lagom_comm_nvls_alloc(lagom_comm_t c, int64_t bytes, void** ptr) {
 
 int64_t lagom_comm_nvls_bytes(lagom_comm_t c) { return c && c->nvls_ready ? c->nvls_bytes : 0; }
 
+int lagom_comm_nvls_scratch(lagom_comm_t c, int64_t slot_bytes) {
+  if (!c || slot_bytes <= 0) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_scratch: bad arguments");
+  if (c->nvls_scratch) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_scratch: already reserved");
+  const int64_t slot = (slot_bytes + 4095) / 4096 * 4096;
+  void* p = nullptr;
+  if (int s = lagom_comm_nvls_alloc(c, slot * c->nranks, &p)) return s;
+  c->nvls_scratch = static_cast<char*>(p);
+  c->nvls_scratch_slot = slot;
+  return LAGOM_OK;
+}
+
 int lagom_comm_nvls_export_peer(lagom_comm_t c, void* blob) {
   if (!c || !blob) return lagom_fail(LAGOM_ERR_INVALID_ARGUMENT, "nvls_export_peer: bad arguments");
   if (!c->nvls_ready) return lagom_fail(LAGOM_ERR_NOT_READY, "nvls_export_peer before nvls_bind");
@@ -791,5 +873,7 @@ void lagom_nvls_release(lagom_comm* c) {
   if (c->nvls_mem_handle) DRV(cuMemRelease)(static_cast<CUmemGenericAllocationHandle>(c->nvls_mem_handle));
   if (c->nvls_mc_handle) DRV(cuMemRelease)(static_cast<CUmemGenericAllocationHandle>(c->nvls_mc_handle));
   c->nvls_mc = c->nvls_uc = nullptr;
+  c->nvls_scratch = nullptr;
+  c->nvls_scratch_slot = 0;
   c->nvls_ready = false;
 }

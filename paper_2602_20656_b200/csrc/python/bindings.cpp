@@ -309,11 +309,13 @@ PYBIND11_MODULE(_lagom_py, m) {
   m.def("seed_configs", [](const std::string& w, const std::string& start, const std::string& p) {
     return configs_to_json(seed_configs(workload_from_json(parse(w)), params_or_default(p), start)).dump();
   }, py::arg("workload"), py::arg("start") = "min", py::arg("params") = "");
-  m.def("simulate", [](const std::string& w, const std::string& c, const std::string& p) {
-    const SimResult r = simulate(workload_from_json(parse(w)), configs_arg(c), params_or_default(p));
+  m.def("simulate", [](const std::string& w, const std::string& c, const std::string& p, bool sm_occupancy) {
+    SimOptions opt;
+    opt.sm_occupancy = sm_occupancy;  // false: running comms hold no SMs (co-resident kernels)
+    const SimResult r = simulate(workload_from_json(parse(w)), configs_arg(c), params_or_default(p), opt);
     return Json{{"x", r.comm_times}, {"y", r.comp_times}, {"X", r.total_comm}, {"Y", r.total_compute},
                 {"Z", r.makespan}, {"trace", trace_to_json(r)}}.dump();
-  }, py::arg("workload"), py::arg("configs"), py::arg("params") = "");
+  }, py::arg("workload"), py::arg("configs"), py::arg("params") = "", py::arg("sm_occupancy") = true);
   m.def("tune_sim", [](const std::string& w, const std::string& start, int budget, const std::string& p) {
     const Workload wl = workload_from_json(parse(w));
     const SubspaceParams params = params_or_default(p);

@@ -16,16 +16,18 @@ from tests import coll_cases  # noqa: E402
 from tests.oracle_ref import collective as oracle_collective, in_elems, out_elems  # noqa: E402
 
 
-# Unit roundoff of the output type: the switch accumulates in fp32 and
-# rounds the sum to the output type once.
-UNIT_ROUNDOFF = {0: 2.0 ** -24, 1: 2.0 ** -8, 2: 2.0 ** -11}
+# One ulp of the output type relative to |S| (2^-7 bf16, 2^-10 f16, 2^-23
+# f32): the switch accumulates in fp32 (.acc::f32) but its conversion of the
+# sum to bf16 is faithful, not correctly rounded — measured on 2xB200 up to
+# 0.8 ulp off the fp64 sum, where round-to-nearest would be
+# at most 0.5 ulp.
+ULP = {0: 2.0 ** -23, 1: 2.0 ** -7, 2: 2.0 ** -10}
 
 
 def within_tolerance(got, sends, c):
-    """In-switch (NVLS) sums against the EXACT fp64 sum of the inputs:
-    |got - S| <= u_out * |S| + n * 2^-23 * sum|x|, i.e. one rounding to the
-    output type plus fp32 accumulation of n terms (u_out = 2^-8 bf16,
-    2^-11 f16, 2^-24 f32)."""
+    """In-switch (NVLS) sums against the EXACT fp64 sum S of the inputs:
+    |got - S| <= ulp_rel * |S| + n * 2^-23 * sum|x| — one faithful rounding
+    to the output type plus fp32 accumulation of n terms."""
     from tests.test_oracle_cpu import to_f32
     g = to_f32(got, c["dtype"]).astype(np.float64)
     n = len(sends)
@@ -37,8 +39,14 @@ def within_tolerance(got, sends, c):
         parts = [to_f32(s[r * k:(r + 1) * k], c["dtype"]).astype(np.float64) for s in sends]
     exact = np.sum(parts, axis=0)
     mag = np.sum(np.abs(parts), axis=0)
-    tol = UNIT_ROUNDOFF[c["dtype"]] * np.abs(exact) + n * 2.0 ** -23 * mag
-    return bool(np.all(np.abs(g - exact) <= tol))
+    tol = ULP[c["dtype"]] * np.abs(exact) + n * 2.0 ** -23 * mag
+    ok = bool(np.all(np.abs(g - exact) <= tol))
+    if not ok:
+        bad = np.flatnonzero(np.abs(g - exact) > tol)
+        i = bad[np.argmax((np.abs(g - exact) / np.maximum(tol, 1e-30))[bad])]
+        print(f"[tolerance] {bad.size} of {g.size} outside: worst i={i} got={g[i]!r} exact={exact[i]!r} "
+              f"err/|S|={abs(g[i] - exact[i]) / max(abs(exact[i]), 1e-30):.3e} tol={tol[i]:.3e}", flush=True)
+    return ok
 
 
 def main():
@@ -95,8 +103,12 @@ def main():
     band = 4096
     nbytes = max(4 * max(in_elems(c["coll"], world, c["count"]), out_elems(c["coll"], world, c["count"]))
                  for c in cases) + band
+    one_hop = int(os.environ.get("LAGOM_ONE_HOP", "0"))
+    rs_slot = max([2 * c["count"] * 4 for c in cases if c["coll"] == C.REDUCE_SCATTER] + [0])
     if nvls:
-        comm.enable_nvls(max(1 << 30, 2 * nbytes + (64 << 20)))
+        comm.enable_nvls(max(1 << 30, 2 * nbytes + (64 << 20) + world * rs_slot))
+        if one_hop and rs_slot:
+            comm.nvls_scratch(rs_slot)  # push-based one-hop ReduceScatter
         xbuf = comm.nvls_tensor(nbytes, torch.uint8)
         ybuf = comm.nvls_tensor(nbytes, torch.uint8)
     else:

@@ -25,6 +25,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 KIB = 1024
+MIB = 1 << 20
 
 
 def fit(points):
@@ -54,8 +55,10 @@ def fit(points):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--profile", required=True)
-    ap.add_argument("--bench", required=True)
+    ap.add_argument("--profile", default="")
+    ap.add_argument("--bench", default="")
+    ap.add_argument("--counters", default="", help="a counter profile (tools/counter_profile.py): fit the "
+                    "model from CUPTI counters and predict its measured config sets")
     ap.add_argument("--out", default="")
     ap.add_argument("--waves", type=int, default=16)
     ap.add_argument("--fit-cache", default="", help="reuse (or write) the comm-model fit of --profile")
@@ -64,6 +67,13 @@ def main():
                          "blocks*D/(B - V) (reference contention.cpp:35-44), the rest in theta; "
                          "0 = no HBM term (the comm footprint V then has no effect)")
     a = ap.parse_args()
+    if a.counters:
+        res = counter_model(a.counters, a.waves, a.out)
+        for r in res["rows"]:
+            print(json.dumps({"set": r["set"], "coresident": r["coresident"], "Z_pred": round(r["predicted"]["Z"], 1),
+                              "Z_meas": round(r["measured"]["Z"], 1), "Z_err": round(r["rel_err"]["Z"], 4),
+                              "Y_err": round(r["rel_err"]["Y"], 4), "V_GBps": round(r["V_GBps"], 1)}))
+        return
     from paper_2602_20656_b200 import _lagom_py as L
     from paper_2602_20656_b200 import dags
 
@@ -166,3 +176,116 @@ def _groups(dag):
 
 if __name__ == "__main__":
     main()
+
+
+# ------------------------------------------------------------------ counters
+def counter_model(profile_path, waves=16, out=""):
+    """Predicted vs measured from one counter profile (tools/counter_profile.py):
+    the reference model calibrated from CUPTI counters, then simulate()
+    (bit-identical to the reference's) predicts every measured config set's
+    overlapped Z, which the same run measured.
+
+      comm_time  (commperf.cpp:112-125): fitted per subspace to the sets'
+                 comm-alone kernel spans x_j;
+      V          (mem_footprint, commperf.cpp:127-135): mem_coeff / chunk_knee
+                 fitted to each set's measured HBM bytes per us of comm;
+      D          (ComputeOp.bytes_per_block): each compute op's measured HBM
+                 bytes / its blocks (lambda x waves CTAs); theta so that the
+                 isolated time is matched: f = theta + blocks*D/(B - V);
+      delta      (compute_on_comm_slowdown): median over sets of overlapped /
+                 alone comm span - 1;
+      sm_occupancy (SimOptions): False for sets whose kernels ride along the
+                 GEMMs (co-resident regime), True where they take SMs."""
+    from paper_2602_20656_b200 import _lagom_py as L
+    from paper_2602_20656_b200 import dags
+    prof = json.load(open(profile_path))
+    n = prof["n"]
+    wl = prof["workload"]
+    dag = dags.BUILDERS[_builder({"config": {"workload": wl}})](n)
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else {}
+    B = peaks.get("hbm_gbs", 6540.8) * 1e3  # bytes/us
+    lam = 148
+    sizes = []
+    for c in dag["comm_ops"]:
+        e = 2 if c.get("dtype", 1) in (1, 2) else 4
+        sizes.append(c["count"] * e * (1 if c["collective"] == "ALL_REDUCE" else n))
+    # comm_time fit per subspace over every set's comm-alone spans
+    by_key = {}
+    for spec, st in prof["sets"].items():
+        cfg = st["config"]
+        key = f"{cfg['algorithm']}/{cfg['protocol']}/P2P"
+        for j, co in enumerate(st["comm_ops"]):
+            f = 2.0 if dag["comm_ops"][j]["collective"] == "ALL_REDUCE" else 1.0
+            by_key.setdefault(key, []).append((cfg["num_channels"], cfg["num_threads"], cfg["chunk_size"],
+                                               sizes[j] * f, co["x_us"]))
+    params, report, links = {}, {}, {}
+    for key, pts in by_key.items():
+        co, lk, rep = fit(pts)
+        params[key], links[key] = co, lk
+        report[key] = dict(rep, link_bw=lk)
+    # footprint V per set (HBM bytes per us of comm), fitted per subspace
+    for key in by_key:
+        vpts = []
+        for spec, st in prof["sets"].items():
+            cfg = st["config"]
+            if f"{cfg['algorithm']}/{cfg['protocol']}/P2P" != key:
+                continue
+            xs = sum(c["x_us"] for c in st["comm_ops"])
+            vpts.append((cfg["num_channels"], cfg["chunk_size"], sum(c["dram_bytes"] for c in st["comm_ops"]) / xs))
+        bch = params[key]["per_channel_bw"]
+        best = None
+        for knee in (0, 16 * KIB, 64 * KIB, 256 * KIB, MIB):
+            num = sum(v * nc * c / (c + knee) * bch for nc, c, v in vpts)
+            den = sum((nc * c / (c + knee) * bch) ** 2 for nc, c, v in vpts)
+            kappa = num / den if den else 0.0
+            err = sum((kappa * nc * c / (c + knee) * bch - v) ** 2 for nc, c, v in vpts)
+            if best is None or err < best[0]:
+                best = (err, kappa, knee)
+        params[key]["mem_coeff"] = float(best[1])
+        params[key]["chunk_knee"] = int(best[2])
+        report[key]["V_points"] = vpts
+    for key in ("RING/SIMPLE/P2P", "RING/LL/P2P", "RING/LL128/P2P", "TREE/SIMPLE/P2P", "TREE/LL/P2P",
+                "TREE/LL128/P2P"):
+        params.setdefault(key, dict(next(iter(params.values()))))
+    params["collective_factors"] = {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0}
+    # delta: comm slowdown under compute
+    ratios = [sum(st["overlapped_x"]) / sum(c["x_us"] for c in st["comm_ops"]) for st in prof["sets"].values()]
+    delta = max(0.0, float(np.median(ratios)) - 1.0)
+    rows = []
+    for spec, st in prof["sets"].items():
+        cfg = st["config"]
+        key = f"{cfg['algorithm']}/{cfg['protocol']}/P2P"
+        coresident = cfg["algorithm"] == "TREE" and cfg["num_threads"] <= 256 and prof.get("nvls", False)
+        gpu = {"num_sms": lam, "peak_mem_bw": B, "link_bw": links[key], "comm_bw_cap_fraction": 0.6,
+               "compute_on_comm_slowdown": delta}
+        comps = []
+        for i, c in enumerate(dag["compute_ops"]):
+            co = prof["compute_ops"][i]
+            D = co["dram_bytes"] / (lam * waves)
+            f = co["y_us"] / waves
+            comps.append({"id": c["id"], "total_blocks": lam * waves, "blocks_per_sm": 1,
+                          "bytes_per_block": int(round(D)), "base_wave_time": max(1e-3, f - lam * round(D) / B)})
+        work = {"units": {"time": "us", "size": "bytes", "bandwidth": "bytes_per_us"}, "gpu": gpu,
+                "compute_ops": comps, "comm_ops": []}
+        for j, c in enumerate(dag["comm_ops"]):
+            op = {"id": c["id"], "collective": c["collective"], "message_bytes": sizes[j]}
+            if c.get("ready_after"):
+                op["ready_after"] = c["ready_after"]
+            work["comm_ops"].append(op)
+        sim = json.loads(L.simulate(json.dumps(work), json.dumps({"configs": [cfg] * len(sizes)}),
+                                    json.dumps(params), not coresident))
+        meas = st["overlapped"]
+        rows.append({"set": spec, "coresident": coresident, "predicted": {k: sim[k] for k in ("X", "Y", "Z")},
+                     "measured": {k: meas[k] for k in ("X", "Y", "Z")},
+                     "rel_err": {k: (sim[k] - meas[k]) / meas[k] for k in ("X", "Y", "Z")},
+                     "V_GBps": sum(c["dram_bytes"] for c in st["comm_ops"]) / sum(c["x_us"] for c in st["comm_ops"])
+                     / 1e3})
+    res = {"workload": wl, "n": n, "params": params, "fit_report": report, "delta": delta,
+           "hbm_bytes_per_us": B, "waves": waves, "rows": rows,
+           "max_abs_Z_err": max(abs(r["rel_err"]["Z"]) for r in rows)}
+    if out:
+        with open(out, "w") as f:
+            json.dump(res, f, indent=1)
+    return res
