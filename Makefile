@@ -11,6 +11,13 @@
 # its doubles round exactly like the reference build (SURVEY finding 2).
 
 PY        ?= python3
+# /usr/bin/g++ links libstdc++ as a shared library. The image's default
+# $(CXX) wrapper (/opt/gcc) embeds a static copy and re-exports it, which
+# clashes with the process's libstdc++ once our libraries share iostreams
+# with torch / cuDNN in one process.
+ifneq ($(wildcard /usr/bin/g++),)
+CXX       := /usr/bin/g++
+endif
 PKG       := paper_2602_20656_b200
 NVCC      ?= nvcc
 CXX       ?= g++
@@ -67,13 +74,19 @@ $(PKG)/liblagom_coll.so: $(CU_OBJS)
 B200_SRCS  := $(wildcard $(PKG)/csrc/b200/*.cpp)
 B200_OBJS  := $(patsubst $(PKG)/csrc/b200/%.cpp,build/b200/%.o,$(B200_SRCS)) build/b200/exhaustive_gpu.o
 CUDA_INC   := -I$(CUDA_HOME)/include
-CUDA_LIBS  := -L$(CUDA_HOME)/lib64 -lcudart -lcublasLt -ldl -lrt
+# cuDNN: the frontend headers and the cuDNN 9 runtime torch ships (one cuDNN
+# per process; the system copy is older than the sm_100 SDPA engines need).
+SITE       := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
+CUDNN_FE   ?= $(SITE)/include
+CUDNN_DIR  ?= $(SITE)/nvidia/cudnn
+CUDA_LIBS  := -L$(CUDA_HOME)/lib64 -lcudart -lcublasLt -L$(CUDNN_DIR)/lib -l:libcudnn.so.9 \
+              -Wl,-rpath,$(CUDNN_DIR)/lib -ldl -lrt
 
 b200: $(PKG)/liblagom_b200.so
 
 build/b200/%.o: $(PKG)/csrc/b200/%.cpp $(wildcard $(PKG)/csrc/b200/*.hpp) $(wildcard include/lagom/*.hpp) include/lagom_coll.h
 	@mkdir -p build/b200
-	$(CXX) $(HOST_FLAGS) $(CUDA_INC) -c $< -o $@
+	$(CXX) $(HOST_FLAGS) $(CUDA_INC) -isystem $(CUDNN_DIR)/include -isystem $(CUDNN_FE) -c $< -o $@
 
 # --fmad=false: the GPU exhaustive oracle must round like the host simulator
 build/b200/exhaustive_gpu.o: $(PKG)/csrc/b200/exhaustive_gpu.cu $(wildcard include/lagom/*.hpp)

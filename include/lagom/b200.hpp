@@ -36,9 +36,18 @@ struct GemmShape {
   std::int64_t batch = 1;            // > 1: strided-batched (attention cores)
 };
 
+// Fused scaled-dot-product attention (cuDNN SDPA, flash-style): Q, K, V
+// [batch, heads, seq, head_dim] bf16, fp32 softmax; forward or backward.
+struct AttentionShape {
+  std::int64_t batch = 1, heads = 1, seq = 0, head_dim = 128;
+  bool causal = true;
+  bool backward = false;
+};
+
 struct ReplayComputeOp {
   std::string id;
-  std::vector<GemmShape> gemms;  // executed back to back on the compute stream
+  std::vector<GemmShape> gemms;           // executed back to back on the compute stream,
+  std::vector<AttentionShape> attention;  // then these
 };
 
 // Element type codes are lagom_dtype_t (include/lagom_coll.h).
@@ -67,6 +76,11 @@ double compute_flops(const ReplayComputeOp& op);
 // The tuner's view of the DAG. Compute ops get wave-model parameters
 // estimated from their GEMM shapes (the contention profiler refits them).
 Workload to_workload(const ReplayDag& dag, const GpuSpec& gpu, int nranks);
+// The replay DAG JSON (paper_2602_20656_b200/dags.py): compute_ops with
+// "gemms" [[m, n, k(, batch)], ...] and "attention" [[batch, heads, seq,
+// head_dim, causal, backward], ...]; comm_ops with collective, dtype, count,
+// ready_after and bounds.
+ReplayDag replay_dag_from_json(const std::string& text);
 
 // ------------------------------------------------------------ coordinator --
 class Coordinator {

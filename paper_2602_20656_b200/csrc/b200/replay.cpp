@@ -22,8 +22,10 @@
 #include <map>
 #include <unordered_map>
 
+#include "attention.hpp"
 #include "lagom/b200.hpp"
 #include "lagom/error.hpp"
+#include "lagom/json_io.hpp"
 #include "lagom_coll.h"
 #include "nccl_dl.hpp"
 
@@ -130,12 +132,55 @@ std::int64_t message_bytes(const ReplayCommOp& op, int nranks) {
   return op.collective == Collective::AllReduce ? op.count * e : op.count * e * nranks;
 }
 
+double attention_flops(const AttentionShape& a) {
+  // forward: QK^T and PV, 2 x 2*b*h*s*s*d; backward 2.5x (dV, dP, dQ, dK + recompute of S);
+  // causal masks half of the score matrix
+  const double fwd = 4.0 * static_cast<double>(a.batch * a.heads) * static_cast<double>(a.seq) *
+                     static_cast<double>(a.seq) * static_cast<double>(a.head_dim) * (a.causal ? 0.5 : 1.0);
+  return a.backward ? 2.5 * fwd : fwd;
+}
+
 double compute_flops(const ReplayComputeOp& op) {
   double f = 0;
   for (const GemmShape& g : op.gemms)
     f += 2.0 * static_cast<double>(g.m) * static_cast<double>(g.n) * static_cast<double>(g.k) *
          static_cast<double>(g.batch);
+  for (const AttentionShape& a : op.attention) f += attention_flops(a);
   return f;
+}
+
+ReplayDag replay_dag_from_json(const std::string& text) {
+  const Json d = parse_json(text, "dag");
+  ReplayDag dag;
+  dag.name = d.value("name", std::string("dag"));
+  for (const Json& c : d.at("compute_ops")) {
+    ReplayComputeOp op;
+    op.id = c.at("id").get<std::string>();
+    for (const Json& g : c.value("gemms", Json::array()))
+      op.gemms.push_back({g.at(0).get<std::int64_t>(), g.at(1).get<std::int64_t>(), g.at(2).get<std::int64_t>(),
+                          g.size() > 3 ? g.at(3).get<std::int64_t>() : 1});
+    for (const Json& a : c.value("attention", Json::array()))
+      op.attention.push_back({a.at(0).get<std::int64_t>(), a.at(1).get<std::int64_t>(), a.at(2).get<std::int64_t>(),
+                              a.at(3).get<std::int64_t>(), a.size() > 4 ? a.at(4).get<int>() != 0 : true,
+                              a.size() > 5 ? a.at(5).get<int>() != 0 : false});
+    dag.compute_ops.push_back(op);
+  }
+  for (const Json& c : d.at("comm_ops")) {
+    ReplayCommOp op;
+    op.id = c.at("id").get<std::string>();
+    op.collective = collective_from_string(c.at("collective").get<std::string>());
+    op.dtype = c.value("dtype", 1);
+    op.count = c.at("count").get<std::int64_t>();
+    if (c.contains("ready_after") && !c["ready_after"].is_null()) op.ready_after = c["ready_after"].get<std::string>();
+    if (c.contains("bounds")) {
+      const Json& b = c["bounds"];
+      op.bounds.nc_max = b.value("nc_max", op.bounds.nc_max);
+      op.bounds.c_min = b.value("c_min", op.bounds.c_min);
+      op.bounds.c_max = b.value("c_max", op.bounds.c_max);
+    }
+    dag.comm_ops.push_back(op);
+  }
+  return dag;
 }
 
 Workload to_workload(const ReplayDag& dag, const GpuSpec& gpu, int nranks) {
@@ -154,6 +199,10 @@ Workload to_workload(const ReplayDag& dag, const GpuSpec& gpu, int nranks) {
       tiles += ((g.m + 255) / 256) * ((g.n + 127) / 128) * g.batch;
       bytes += 2.0 * static_cast<double>(g.batch) *
                static_cast<double>(g.m * g.k + g.k * g.n + g.m * g.n);
+    }
+    for (const AttentionShape& a : c.attention) {  // one CTA per 128-row query tile
+      tiles += a.batch * a.heads * ((a.seq + 127) / 128);
+      bytes += 2.0 * static_cast<double>(a.batch * a.heads * a.seq * a.head_dim) * (a.backward ? 8.0 : 4.0);
     }
     op.total_blocks = std::max<std::int64_t>(1, tiles);
     op.blocks_per_sm = 1;
@@ -187,6 +236,10 @@ struct ReplayEngine::Impl {
   void* workspace = nullptr;
   std::size_t workspace_bytes = 64ull << 20;
   std::vector<std::vector<Gemm>> gemms;  // per compute op
+  void* cudnn = nullptr;                 // cuDNN handle (attention victims)
+  std::vector<std::unique_ptr<Attention>> attn_pool;  // one per distinct shape (shared by layers)
+  std::vector<std::vector<Attention*>> attention;     // per compute op
+  void* attn_workspace = nullptr;
   std::map<std::tuple<std::int64_t, std::int64_t, std::int64_t, std::int64_t>, std::array<void*, 3>> operands;
   std::vector<Comm> comms;
   lagom_comm_t lcomm = nullptr;
@@ -215,6 +268,7 @@ struct ReplayEngine::Impl {
     lt_check(cublasLtCreate(&lt), "cublasLtCreate");
     cuda_check(cudaMalloc(&workspace, workspace_bytes), "workspace");
     build_gemms();
+    build_attention();
     build_comm_backends();
     build_comms();
     auto mk = [](cudaEvent_t* e) { cuda_check(cudaEventCreate(e), "event"); };
@@ -264,6 +318,10 @@ struct ReplayEngine::Impl {
       }
     for (auto& [k, p] : operands)
       for (void* q : p) cudaFree(q);
+    attention.clear();
+    attn_pool.clear();
+    if (attn_workspace) cudaFree(attn_workspace);
+    destroy_cudnn_handle(cudnn);
     for (Comm& c : comms) {
       if (c.nvls) continue;  // owned by the communicator's NVLS region
       cudaFree(c.send);
@@ -349,6 +407,29 @@ struct ReplayEngine::Impl {
         gemms[i].push_back(g);
       }
     }
+  }
+
+  void build_attention() {
+    attention.resize(dag.compute_ops.size());
+    std::int64_t ws = 0;
+    for (std::size_t i = 0; i < dag.compute_ops.size(); ++i)
+      for (const AttentionShape& a : dag.compute_ops[i].attention) {
+        if (!cudnn) cudnn = create_cudnn_handle();
+        Attention* hit = nullptr;
+        for (auto& p : attn_pool) {
+          const AttentionShape& s = p->shape();
+          if (s.batch == a.batch && s.heads == a.heads && s.seq == a.seq && s.head_dim == a.head_dim &&
+              s.causal == a.causal && s.backward == a.backward)
+            hit = p.get();
+        }
+        if (!hit) {
+          attn_pool.push_back(std::make_unique<Attention>(a, cudnn, opts.seed * 7777 + attn_pool.size() + 97 * rank, cs));
+          hit = attn_pool.back().get();
+          ws = std::max(ws, hit->workspace_bytes());
+        }
+        attention[i].push_back(hit);
+      }
+    if (ws > 0) cuda_check(cudaMalloc(&attn_workspace, static_cast<std::size_t>(ws)), "attention workspace");
   }
 
   void build_comms() {
@@ -604,6 +685,7 @@ struct ReplayEngine::Impl {
       for (std::size_t i = 0; i < M; ++i) {
         cuda_check(cudaEventRecord(ev_cb[i], cs), "record");
         for (Gemm& g : gemms[i]) launch_gemm(g, sm_target[i]);
+        for (Attention* at : attention[i]) at->launch(cudnn, cs, attn_workspace);
         cuda_check(cudaEventRecord(ev_ce[i], cs), "record");
       }
     }

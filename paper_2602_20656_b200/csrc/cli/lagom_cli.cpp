@@ -330,26 +330,7 @@ std::unique_ptr<GpuSession> gpu_session(const Args& a, const lagom::Workload& w)
   const char* job = std::getenv("LAGOM_JOB");
   const char* port = std::getenv("MASTER_PORT");
   const std::string name = std::string("lagom_cli_") + (job ? job : (port ? port : "0"));
-  const Json dj = lagom::parse_json(lagom::read_file(a.get("dag")), a.get("dag"));
-  lagom::b200::ReplayDag dag;
-  dag.name = dj.value("name", std::string("dag"));
-  for (const Json& c : dj.at("compute_ops")) {
-    lagom::b200::ReplayComputeOp op;
-    op.id = c.at("id").get<std::string>();
-    for (const Json& g : c.at("gemms"))
-      op.gemms.push_back({g.at(0).get<std::int64_t>(), g.at(1).get<std::int64_t>(), g.at(2).get<std::int64_t>(),
-                          g.size() > 3 ? g.at(3).get<std::int64_t>() : 1});
-    dag.compute_ops.push_back(op);
-  }
-  for (const Json& c : dj.at("comm_ops")) {
-    lagom::b200::ReplayCommOp op;
-    op.id = c.at("id").get<std::string>();
-    op.collective = lagom::collective_from_string(c.at("collective").get<std::string>());
-    op.dtype = c.value("dtype", 1);
-    op.count = c.at("count").get<std::int64_t>();
-    if (c.contains("ready_after") && !c["ready_after"].is_null()) op.ready_after = c["ready_after"].get<std::string>();
-    dag.comm_ops.push_back(op);
-  }
+  const lagom::b200::ReplayDag dag = lagom::b200::replay_dag_from_json(lagom::read_file(a.get("dag")));
   if (dag.comm_ops.size() != w.comm_ops.size())
     throw lagom::Error(lagom::ErrorCode::InvalidInput, "dag", "the DAG must have one comm op per workload comm op");
   auto s = std::make_unique<GpuSession>();

@@ -97,36 +97,6 @@ Json tune_json(const Workload& w, const TuneResult& r, double wall_us) {
               {"states", states}};
 }
 
-ReplayDag dag_from_json(const Json& d) {
-  ReplayDag dag;
-  dag.name = d.value("name", std::string("dag"));
-  for (const Json& c : d.at("compute_ops")) {
-    b200::ReplayComputeOp op;
-    op.id = c.at("id").get<std::string>();
-    for (const Json& g : c.at("gemms"))
-      op.gemms.push_back({g.at(0).get<std::int64_t>(), g.at(1).get<std::int64_t>(), g.at(2).get<std::int64_t>(),
-                          g.size() > 3 ? g.at(3).get<std::int64_t>() : 1});
-    dag.compute_ops.push_back(op);
-  }
-  for (const Json& c : d.at("comm_ops")) {
-    b200::ReplayCommOp op;
-    op.id = c.at("id").get<std::string>();
-    op.collective = collective_from_string(c.at("collective").get<std::string>());
-    op.dtype = c.value("dtype", 1);
-    op.count = c.at("count").get<std::int64_t>();
-    if (c.contains("ready_after") && !c["ready_after"].is_null())
-      op.ready_after = c["ready_after"].get<std::string>();
-    if (c.contains("bounds")) {
-      const Json& b = c["bounds"];
-      op.bounds.nc_max = b.value("nc_max", op.bounds.nc_max);
-      op.bounds.c_min = b.value("c_min", op.bounds.c_min);
-      op.bounds.c_max = b.value("c_max", op.bounds.c_max);
-    }
-    dag.comm_ops.push_back(op);
-  }
-  return dag;
-}
-
 GpuSpec gpu_from_json(const std::string& s) {
   GpuSpec g;
   if (s.empty()) return g;
@@ -166,7 +136,7 @@ class PyEngine {
            int repeats, int warmup, bool nccl, std::int64_t max_chunk, int max_channels,
            std::int64_t e2e_in, std::int64_t e2e_out, int sm_partition, bool nvls, bool coresident, int one_hop,
            bool a2a_tma, std::uint64_t pm_interval_ns)
-      : dag_(dag_from_json(parse(dag_json))) {
+      : dag_(b200::replay_dag_from_json(dag_json)) {
     coord_ = b200::make_shm_coordinator(coord_name, rank, size);
     b200::ReplayOptions o;
     o.device = device;

@@ -3,7 +3,8 @@
 Each DAG is the reference Workload's overlap shape (ordered compute stream,
 serialized comm stream, ``ready_after`` gates — reference model.hpp:78-96 and
 the generator shapes of reference workloads.cpp:59-109) with real kernels
-attached: cuBLASLt bf16 GEMMs [m, n, k(, batch)] per compute op, and one
+attached: cuBLASLt bf16 GEMMs [m, n, k(, batch)] and fused cuDNN SDPA
+attention [batch, heads, seq, head_dim, causal, backward] per compute op, and one
 collective per comm op (bf16, counts per include/lagom_coll.h). Shapes follow
 the public model cards; data is synthetic (random-init on device).
 
@@ -20,14 +21,10 @@ BF16 = 1
 MiB = 1 << 20
 
 
-def _attn_bwd(seq, d, heads_x_batch):
-    # dP = dO V^T (s,s,d); dV = P^T dO, dQ = dS K, dK = dS^T Q (s,d,s)
-    return [[seq, seq, d, heads_x_batch], [seq, d, seq, heads_x_batch],
-            [seq, d, seq, heads_x_batch], [seq, d, seq, heads_x_batch]]
-
-
-def _attn_fwd(seq, d, heads_x_batch):
-    return [[seq, seq, d, heads_x_batch], [seq, d, seq, heads_x_batch]]
+def _sdpa(batch, heads, seq, d, backward, causal=True):
+    """A fused attention (cuDNN SDPA, flash-style) entry of a compute op:
+    [batch, heads, seq, head_dim, causal, backward]."""
+    return [batch, heads, seq, d, int(causal), int(backward)]
 
 
 def gpt2_dp(nranks: int, layers: int = 24):
@@ -40,11 +37,11 @@ def gpt2_dp(nranks: int, layers: int = 24):
     gemms = [[T, 4 * h, h], [h, 4 * h, T],       # fc2 dgrad / wgrad
              [T, h, 4 * h], [4 * h, h, T],       # fc1
              [T, h, h], [h, h, T]]               # attention out-proj
-    gemms += _attn_bwd(s, d, heads * mb)          # attention core backward
     gemms += [[T, h, 3 * h], [3 * h, h, T]]      # qkv
+    attention = [_sdpa(mb, heads, s, d, backward=True)]  # attention core backward (fused)
     compute, comm = [], []
     for l in range(layers):
-        compute.append({"id": f"bwd{l}", "gemms": gemms})
+        compute.append({"id": f"bwd{l}", "gemms": gemms, "attention": attention})
         left, b = layer_bytes, 0
         while left > 0:
             nbytes = min(bucket, left)
@@ -68,9 +65,11 @@ def llama8b_tp_sp(nranks: int, layers: int = 32):
     compute, comm = [], []
     for l in range(layers):
         qkv = (q_heads + 2 * kv_heads) * hd // n
-        attn = [[T, qkv, h]] + _attn_fwd(T, hd, max(1, q_heads // n)) + [[T, h, q_heads * hd // n]]
+        attn = [[T, qkv, h], [T, h, q_heads * hd // n]]
         mlp = [[T, 2 * ffn // n, h], [T, h, ffn // n]]
-        compute.append({"id": f"attn{l}", "gemms": attn})
+        # this rank's q heads, causal, full sequence (K/V expanded to the q heads)
+        compute.append({"id": f"attn{l}", "gemms": attn,
+                        "attention": [_sdpa(1, max(1, q_heads // n), T, hd, backward=False)]})
         compute.append({"id": f"mlp{l}", "gemms": mlp})
         comm.append({"id": f"rs_attn{l}", "collective": "REDUCE_SCATTER", "dtype": BF16,
                      "count": shard * h, "ready_after": f"attn{l}", "role": 0})
@@ -95,13 +94,12 @@ def llama70b_fsdp(nranks: int, layers: int = 4):
     shard = layer_params // n
     compute, comm = [], []
     for l in range(layers):
-        g = [[T, (q_heads + 2 * kv_heads) * hd, h]] + _attn_fwd(T, hd, q_heads) + \
-            [[T, h, q_heads * hd], [T, 2 * ffn, h], [T, h, ffn]]
+        g = [[T, (q_heads + 2 * kv_heads) * hd, h], [T, h, q_heads * hd], [T, 2 * ffn, h], [T, h, ffn]]
         ag = {"id": f"ag{l}", "collective": "ALL_GATHER", "dtype": BF16, "count": shard, "role": 0}
         if l > 0:
             ag["ready_after"] = f"layer{l - 1}"
         comm.append(ag)
-        compute.append({"id": f"layer{l}", "gemms": g})
+        compute.append({"id": f"layer{l}", "gemms": g, "attention": [_sdpa(1, q_heads, T, hd, backward=False)]})
         comm.append({"id": f"rs{l}", "collective": "REDUCE_SCATTER", "dtype": BF16, "count": shard,
                      "ready_after": f"layer{l}", "role": 1})
     return {"name": f"llama3-70b-layers-fsdp{n}", "parallelism": f"fsdp{n}", "compute_ops": compute,
@@ -142,12 +140,23 @@ BUILDERS = {"gpt2-1.3b-dp": gpt2_dp, "llama3-8b-tp-sp": llama8b_tp_sp,
             "llama3-70b-fsdp": llama70b_fsdp, "mixtral-8x7b-ep": mixtral_ep}
 
 
+def attention_flops(a) -> float:
+    """Forward 4*b*h*s^2*d (QK^T and PV), backward 2.5x; causal halves it
+    (replay.cpp attention_flops)."""
+    b, h, s, d = a[0], a[1], a[2], a[3]
+    causal = a[4] if len(a) > 4 else 1
+    bwd = a[5] if len(a) > 5 else 0
+    fwd = 4.0 * b * h * s * s * d * (0.5 if causal else 1.0)
+    return 2.5 * fwd if bwd else fwd
+
+
 def flops(dag: dict) -> float:
     tot = 0.0
     for c in dag["compute_ops"]:
         for g in c["gemms"]:
             b = g[3] if len(g) > 3 else 1
             tot += 2.0 * g[0] * g[1] * g[2] * b
+        tot += sum(attention_flops(a) for a in c.get("attention", []))
     return tot
 
 

@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--interval-ns", type=int, default=20000)
     ap.add_argument("--nvls", type=int, default=1)
     ap.add_argument("--sm-partition", type=int, default=1)
+    ap.add_argument("--one-hop", type=int, default=2, help="lagom_comm_opts_t.one_hop (bench.py's default)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     rank, world, local = dist_env()
@@ -71,7 +72,7 @@ def main():
     dag = dags.with_nc_max(dags.BUILDERS[a.workload](world), 64)
     eng = L.ReplayEngine(json.dumps(dag), f"cp_{token}", rank, world, local, repeats=1, warmup=1, nccl=False,
                          sm_partition=a.sm_partition, max_channels=64, nvls=bool(a.nvls),
-                         pm_interval_ns=a.interval_ns)
+                         one_hop=a.one_hop, pm_interval_ns=a.interval_ns)
     if rank != 0:
         eng.serve()
         eng.close()

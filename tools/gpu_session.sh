@@ -1,6 +1,4 @@
 set -x
-timeout 1500 python -m pytest tests/test_coll_multigpu.py -q -m gpu -k "2" -s 2>&1 | grep -E "MISMATCH|mp_coll_check|passed|failed|Error|error" | head -40
-TR2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1"
-for W in gpt2-1.3b-dp llama3-70b-fsdp; do
-timeout 900 $TR2 --master-port 29541 bench.py --gpus 2 --workload $W --steps 10 --out gpurun_out/r2b_n2_$W.json > gpurun_out/r2b_n2_$W.log 2>&1; echo "n2 $W exit $?"
-done
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python bench.py --steps 10 --warmup 3 --out gpurun_out/att_n1.json > gpurun_out/att_n1.log 2>&1; echo "bench rc $?"; tail -c 300 gpurun_out/att_n1.log
