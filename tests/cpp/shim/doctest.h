@@ -5,7 +5,8 @@
 // (TEST_CASE, CHECK/REQUIRE and their _FALSE/_MESSAGE/_THROWS_AS/_NOTHROW
 // forms, FAIL, doctest::Approx(...).epsilon(...)) so those suites compile
 // UNMODIFIED from /root/reference/proj/tests against the product library:
-// the drop-in API turns them into a conformance suite (tests/test_conformance.py).
+// the drop-in API turns them into a conformance suite (tests/test_parity_cpu.py,
+// built by tests/cpp/Makefile).
 #pragma once
 
 #include <cmath>

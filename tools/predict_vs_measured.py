@@ -174,9 +174,6 @@ def _groups(dag):
     return [present.index(x) for x in g]
 
 
-if __name__ == "__main__":
-    main()
-
 
 # ------------------------------------------------------------------ counters
 def counter_model(profile_path, waves=16, out=""):
@@ -236,7 +233,7 @@ def counter_model(profile_path, waves=16, out=""):
             vpts.append((cfg["num_channels"], cfg["chunk_size"], sum(c["dram_bytes"] for c in st["comm_ops"]) / xs))
         bch = params[key]["per_channel_bw"]
         best = None
-        for knee in (0, 16 * KIB, 64 * KIB, 256 * KIB, MIB):
+        for knee in (KIB, 16 * KIB, 64 * KIB, 256 * KIB, MIB):
             num = sum(v * nc * c / (c + knee) * bch for nc, c, v in vpts)
             den = sum((nc * c / (c + knee) * bch) ** 2 for nc, c, v in vpts)
             kappa = num / den if den else 0.0
@@ -270,7 +267,7 @@ def counter_model(profile_path, waves=16, out=""):
         work = {"units": {"time": "us", "size": "bytes", "bandwidth": "bytes_per_us"}, "gpu": gpu,
                 "compute_ops": comps, "comm_ops": []}
         for j, c in enumerate(dag["comm_ops"]):
-            op = {"id": c["id"], "collective": c["collective"], "message_bytes": sizes[j]}
+            op = {"id": c["id"], "collective": c["collective"], "message_bytes": sizes[j], "bounds": {"nc_max": 64}}
             if c.get("ready_after"):
                 op["ready_after"] = c["ready_after"]
             work["comm_ops"].append(op)
@@ -289,3 +286,7 @@ def counter_model(profile_path, waves=16, out=""):
         with open(out, "w") as f:
             json.dump(res, f, indent=1)
     return res
+
+
+if __name__ == "__main__":
+    main()
