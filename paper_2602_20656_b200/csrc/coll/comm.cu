@@ -71,6 +71,10 @@ void layout(lagom_comm* c) {
   off += ch * n * 128;
   c->off_nvep = off;   // NVLS per-channel epoch (local)
   off += ch * 8;
+  c->off_nvpiece = off;  // push RS: pieces landed [ch][src], 128 B apart (written by src)
+  off += ch * n * 128;
+  c->off_nvpbase = off;  // push RS: pieces completed per channel so far (local)
+  off += ch * 8;
   off = (off + 4095) / 4096 * 4096;
   c->off_slots = off;
   off += ch * n * c->opts.steps * c->slot_bytes;

@@ -35,6 +35,7 @@ struct lagom_comm {
   int64_t nvls_scratch_slot = 0;
   bool nvls_ready = false;
   int64_t off_nvbar = 0, off_nvep = 0;      // NVLS barrier flags / epochs in the heap
+  int64_t off_nvpiece = 0, off_nvpbase = 0; // push RS piece flags / per-channel piece counts
   int nvls_export_fd = -1;                  // rank 0's exported fd, closed once bound
   // Peer (unicast) mappings of every rank's region: one-hop AllToAll writes
   // straight into the destination rank's recv buffer.

@@ -89,6 +89,8 @@ struct NvlsParams {
   char* send_mc;        // multicast views (send/recv inside the NVLS region)
   char* recv_mc;
   int64_t off_nvbar, off_nvep;
+  int64_t off_nvpiece, off_nvpbase;        // push RS: piece flags [ch][src], piece count [ch]
+  int64_t piece_units;                     // push RS: 16 B units per pipelined piece (chunk C)
   unsigned int* abort_flag;
   uint64_t timeout_ns;
   unsigned long long* span;
@@ -256,28 +258,96 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
       }
     }
   } else if constexpr (KIND == 6) {
-    // Push-based one-hop ReduceScatter, phase 1: my partial of every other
-    // rank's block goes straight into that rank's scratch slot for me (one
-    // posted NVLink write per byte, no round trip). Phase 2 runs after the
-    // mid barrier below.
-    for (int k = 1; k < n; ++k) {
-      const int p = (r + k) % n;
-      const uint4* src = reinterpret_cast<const uint4*>(P.send_uc + static_cast<int64_t>(p) * units * 16) + lo;
-      uint4* dst = reinterpret_cast<uint4*>(P.peer_recv[p]) + lo;
-      int64_t left = hi - lo - threadIdx.x;
-      src += threadIdx.x;
-      dst += threadIdx.x;
-      for (; left > (U - 1) * nt; left -= U * nt) {
-        uint4 v[U];
+    // Push-based one-hop ReduceScatter, pipelined in pieces of C bytes (the
+    // config's chunk): my partial of piece i of every other rank's block goes
+    // straight into that rank's scratch slot for me (posted NVLink writes, no
+    // round trip), then a flag per (channel, source) counts the pieces that
+    // landed; the owner reduces piece i in the ring order — acc = x_{r+1},
+    // then x_{r+2}, ..., ending with its own x_r, rounding to the element
+    // type at every combine — as soon as every peer's piece i is there, so
+    // the result is bit-identical to the ring schedule and its oracle. Piece
+    // i+1 is pushed before piece i is reduced.
+    using R = lagom_dev::Red<T, LAGOM_SUM>;
+    __shared__ int s_go;
+    const int64_t pu = P.piece_units > 0 ? P.piece_units : 1;
+    const int64_t npieces = (hi - lo + pu - 1) / pu;
+    uint64_t* pbase_home = reinterpret_cast<uint64_t*>(P.heap[r] + P.off_nvpbase + static_cast<int64_t>(ch) * 8);
+    const uint64_t pbase = *reinterpret_cast<volatile uint64_t*>(pbase_home);
+    const char* own = P.send_uc + static_cast<int64_t>(r) * units * 16;
+    auto part = [&](int q) -> const uint4* {
+      return reinterpret_cast<const uint4*>(q == r ? own : P.scratch + static_cast<int64_t>(q) * P.scratch_slot);
+    };
+    auto push = [&](int64_t i) {
+      const int64_t a = lo + i * pu, b = lagom_dev::lmin(hi, a + pu);
+      for (int k = 1; k < n; ++k) {
+        const int p = (r + k) % n;
+        const uint4* src = reinterpret_cast<const uint4*>(P.send_uc + static_cast<int64_t>(p) * units * 16) + a;
+        uint4* dst = reinterpret_cast<uint4*>(P.peer_recv[p]) + a;
+        int64_t left = b - a - threadIdx.x;
+        src += threadIdx.x;
+        dst += threadIdx.x;
+        for (; left > (U - 1) * nt; left -= U * nt) {
+          uint4 v[U];
 #pragma unroll
-        for (int j = 0; j < U; ++j) v[j] = src[j * nt];
+          for (int j = 0; j < U; ++j) v[j] = src[j * nt];
 #pragma unroll
-        for (int j = 0; j < U; ++j) dst[j * nt] = v[j];
-        src += U * nt;
-        dst += U * nt;
+          for (int j = 0; j < U; ++j) dst[j * nt] = v[j];
+          src += U * nt;
+          dst += U * nt;
+        }
+        for (; left > 0; left -= nt, src += nt, dst += nt) *dst = *src;
       }
-      for (; left > 0; left -= nt, src += nt, dst += nt) *dst = *src;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();  // the piece's peer stores before its flag
+        for (int k = 1; k < n; ++k) {
+          const int p = (r + k) % n;
+          st_release_sys(reinterpret_cast<uint64_t*>(P.heap[p] + P.off_nvpiece + (static_cast<int64_t>(ch) * n + r) * 128),
+                         pbase + static_cast<uint64_t>(i) + 1);
+        }
+      }
+    };
+    if (npieces > 0) push(0);
+    for (int64_t i = 0; i < npieces; ++i) {
+      if (i + 1 < npieces) push(i + 1);
+      if (threadIdx.x == 0) {  // every peer's piece i landed in my scratch
+        bool ok = true;
+        for (int k = 1; k < n && ok; ++k) {
+          const int q = (r + k) % n;
+          ok = nv_wait(reinterpret_cast<const uint64_t*>(P.heap[r] + P.off_nvpiece + (static_cast<int64_t>(ch) * n + q) * 128),
+                       pbase + static_cast<uint64_t>(i) + 1, P);
+        }
+        s_go = ok ? 1 : 0;
+      }
+      __syncthreads();
+      if (!s_go) return;
+      const int64_t a = lo + i * pu, b = lagom_dev::lmin(hi, a + pu);
+      uint4* out = reinterpret_cast<uint4*>(P.recv_uc);
+      for (int64_t u = a + threadIdx.x; u < b; u += nt * U) {
+        uint4 acc[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u + j * nt < b) acc[j] = part((r + 1) % n)[u + j * nt];
+        for (int k = 2; k <= n; ++k) {
+          const uint4* x = part((r + k) % n);
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (u + j * nt < b) acc[j] = lagom_dev::red4<R>(x[u + j * nt], acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (u + j * nt < b) out[u + j * nt] = acc[j];
+      }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *reinterpret_cast<volatile uint64_t*>(pbase_home) = pbase + static_cast<uint64_t>(npieces);
+      // No exit barrier: my output is mine alone, and the next launch's entry
+      // barrier keeps peers from overwriting my scratch while I still read it.
+      *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+      if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+    }
+    return;
   } else if constexpr (KIND == 5) {
     // One-hop ReduceScatter: pull block r of every rank's send through the
     // peer mappings and combine in the ring order (x_{r+1}, then x_{r+2}, ...,
@@ -370,42 +440,9 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();  // my multimem / peer stores are visible everywhere
-    // AR / AG / RS / A2A: nobody reads results or reuses inputs early. Push
-    // RS: every peer's partial for my block has landed in my scratch (the
-    // next launch's entry barrier keeps peers from overwriting it while I
-    // reduce below).
+    // nobody reads results or reuses inputs early
     s_ok = nv_barrier(P, ch, ep + 1) ? 1 : 0;
     if (s_ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
-  }
-  if constexpr (KIND == 6) {
-    // Phase 2: reduce my block in the ring order — acc = x_{r+1}, then
-    // x_{r+2}, ..., ending with my own x_r, every combine rounding to the
-    // element type — so the result is bit-identical to the ring schedule
-    // and its oracle. Peers' partials are local now (scratch slot q).
-    __syncthreads();
-    if (s_ok) {
-      using R = lagom_dev::Red<T, LAGOM_SUM>;
-      const char* own = P.send_uc + static_cast<int64_t>(r) * units * 16;
-      auto part = [&](int q) -> const uint4* {
-        return reinterpret_cast<const uint4*>(q == r ? own : P.scratch + static_cast<int64_t>(q) * P.scratch_slot);
-      };
-      uint4* out = reinterpret_cast<uint4*>(P.recv_uc);
-      for (int64_t u = lo + threadIdx.x; u < hi; u += nt * U) {
-        uint4 acc[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-          if (u + j * nt < hi) acc[j] = part((r + 1) % n)[u + j * nt];
-        for (int k = 2; k <= n; ++k) {
-          const uint4* x = part((r + k) % n);
-#pragma unroll
-          for (int j = 0; j < U; ++j)
-            if (u + j * nt < hi) acc[j] = lagom_dev::red4<R>(x[u + j * nt], acc[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-          if (u + j * nt < hi) out[u + j * nt] = acc[j];
-      }
-    }
   }
   if (threadIdx.x == 0 && P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
 }
@@ -633,6 +670,9 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   }
   p.off_nvbar = c->off_nvbar;
   p.off_nvep = c->off_nvep;
+  p.off_nvpiece = c->off_nvpiece;
+  p.off_nvpbase = c->off_nvpbase;
+  p.piece_units = a->chunk_bytes / 16;
   p.abort_flag = c->abort_dev;
   p.timeout_ns = static_cast<uint64_t>(c->opts.timeout_ms) * 1000000ull;
   p.span = static_cast<unsigned long long*>(a->span_out);

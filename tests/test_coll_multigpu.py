@@ -66,15 +66,17 @@ def test_real_multigpu_parity_one_hop_allgather_reducescatter(world):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("one_hop", [0, 1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_real_multigpu_parity_bench_sizes(world):
+def test_real_multigpu_parity_bench_sizes(world, one_hop):
     """The bench's own collectives at BASELINE sizes on real peers with NVLS
-    on (TREE = in-switch AR/AG/RS, one-hop A2A; RING = P2P rings), NC 8/16,
-    NT 512, C 2 MiB: bit-exact, or within the fp64-exact-sum bound for the
-    switch's fp32 sums."""
+    on (TREE = in-switch AR/AG/RS, or with one_hop the peer-store AllGather
+    and the pipelined push ReduceScatter; one-hop A2A; RING = P2P rings),
+    NC 8/16, NT 512, C 2 MiB: bit-exact, or within the fp64-exact-sum bound
+    for the switch's fp32 sums."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_BENCH_SIZES="1")
+    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_BENCH_SIZES="1", LAGOM_ONE_HOP=str(one_hop))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]

@@ -90,19 +90,25 @@ def main():
             res.append((m, s))
         return res
 
-    # 1. compute only: y_i and HBM bytes per compute op
-    comp = runs(eng.run_compute_only, a.reps)
-    for i, c in enumerate(dag["compute_ops"]):
-        rows = [op_rows(s, "compute")[i] for _, s in comp]
-        out["compute_ops"].append({"id": c["id"], "y_us": med([m["y"][i] for m, _ in comp]),
-                                   "dram_bytes": med([r[DRAM[0]] + r[DRAM[1]] for r in rows]),
-                                   "tensor_active": med([r["sm__pipe_tensor_cycles_active_realtime.avg"]
-                                                         for r in rows]),
-                                   "sm_elapsed": med([r["sm__cycles_elapsed.avg"] for r in rows])})
-    out["compute_Y_us"] = med([m["Y"] for m, _ in comp])
-    out["compute_Z_us"] = med([m["Z"] for m, _ in comp])
-    print(json.dumps({"mode": "compute", "Y_us": out["compute_Y_us"],
-                      "dram_GB": sum(o["dram_bytes"] for o in out["compute_ops"]) / 1e9}), flush=True)
+    # 1. compute only: y_i and HBM bytes per compute op. One replay here and
+    # one after every set below (medians over all of them), so the power-
+    # capped part's clock drift affects the isolated and overlapped
+    # measurements alike.
+    comp = runs(eng.run_compute_only, 1)
+
+    def compute_only_summary():
+        out["compute_ops"] = []
+        for i, c in enumerate(dag["compute_ops"]):
+            rows = [op_rows(s, "compute")[i] for _, s in comp]
+            out["compute_ops"].append({"id": c["id"], "y_us": med([m["y"][i] for m, _ in comp]),
+                                       "dram_bytes": med([r[DRAM[0]] + r[DRAM[1]] for r in rows]),
+                                       "tensor_active": med([r["sm__pipe_tensor_cycles_active_realtime.avg"]
+                                                             for r in rows]),
+                                       "sm_elapsed": med([r["sm__cycles_elapsed.avg"] for r in rows])})
+        out["compute_Y_us"] = med([m["Y"] for m, _ in comp])
+        out["compute_Z_us"] = med([m["Z"] for m, _ in comp])
+        out["compute_replays"] = len(comp)
+
     # 2. per config set: comm alone and overlapped
     for spec in a.sets:
         cfg = parse_cfg(spec)
@@ -133,12 +139,16 @@ def main():
                  "overlapped_y": [med([o["y"][i] for o in ov]) for i in range(len(dag["compute_ops"]))],
                  "overlapped_x": [med([o["x"][j] for o in ov]) for j in range(len(dag["comm_ops"]))]}
         out["sets"][spec] = entry
+        comp += runs(eng.run_compute_only, 1)
         xs = sum(c["x_us"] for c in comm)
         print(json.dumps({"set": spec, "X_alone_us": xs,
                           "V_GBps": sum(c["dram_bytes"] for c in comm) / xs / 1e3,
                           "nvltx_GBps": sum(c["nvltx_bytes"] for c in comm) / xs / 1e3,
                           "Z_over_us": entry["overlapped"]["Z"], "Y_over_us": entry["overlapped"]["Y"]}),
               flush=True)
+    compute_only_summary()
+    print(json.dumps({"mode": "compute", "Y_us": out["compute_Y_us"], "replays": len(comp),
+                      "dram_GB": sum(o["dram_bytes"] for o in out["compute_ops"]) / 1e9}), flush=True)
     eng.set_pm_sampling(False)
     eng.stop()
     eng.close()
