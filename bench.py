@@ -249,7 +249,8 @@ def nccl_log_summary(path: str | None) -> dict:
     return out
 
 
-def wire_bytes(op: dict, n: int, cfg: dict, nvls: bool, one_hop_a2a: bool) -> tuple[float, str]:
+def wire_bytes(op: dict, n: int, cfg: dict, nvls: bool, one_hop_a2a: bool, one_hop_agrs: bool = False
+               ) -> tuple[float, str]:
     """Bytes that cross NVLink per rank, per direction, for one launch of the
     config's schedule, and the schedule's name. n = 1: HBM
     bytes (read + write of the local copy)."""
@@ -259,6 +260,8 @@ def wire_bytes(op: dict, n: int, cfg: dict, nvls: bool, one_hop_a2a: bool) -> tu
     if n == 1:
         return 2.0 * op["count"] * e, "local copy (HBM read + write)"
     tree = cfg["algorithm"] == "TREE"
+    if tree and nvls and one_hop_agrs and coll in ("ALL_GATHER", "REDUCE_SCATTER"):
+        return S * (n - 1) / n, "one hop (peer stores / pushes): (n-1)/n S egress"
     if tree and nvls and coll in ("ALL_REDUCE", "ALL_GATHER", "REDUCE_SCATTER"):
         return float(S), "NVLS (in-switch): S per rank on the busier direction"
     if tree and coll == "ALL_TO_ALL" and one_hop_a2a:
@@ -288,7 +291,7 @@ def main():
                          "collectives whose CTAs cannot share an SM with a GEMM CTA (default), 2 always")
     ap.add_argument("--coresident", type=int, default=1,
                     help="NVLS / one-hop / single-rank kernels sized to co-reside with GEMM CTAs")
-    ap.add_argument("--one-hop", type=int, default=2,
+    ap.add_argument("--one-hop", type=int, default=0,
                     help="lagom_comm_opts_t.one_hop: TREE AG/RS through the switch (0), one hop (1), one hop at n = 2 (2)")
     ap.add_argument("--ablations", type=int, default=1,
                     help="also time: our kernels at the seed with the SM partition forced on, and (N > 1) NCCL "
@@ -459,7 +462,8 @@ def main():
     cfg_dom = full_cfgs[j_dom]
     t_ev = statistics.median(r["x_ev"][j_dom] for r in result["comm"])    # CUDA events, us
     t_span = statistics.median(r["x"][j_dom] for r in result["comm"])     # kernel's own span, us
-    wb, sched = wire_bytes(op, world, cfg_dom, nvls_state["active"], nvls_state["peer_mappings"])
+    one_hop_agrs = nvls_state["peer_mappings"] and (args.one_hop == 1 or (args.one_hop == 2 and world == 2))
+    wb, sched = wire_bytes(op, world, cfg_dom, nvls_state["active"], nvls_state["peer_mappings"], one_hop_agrs)
     e = 2 if op["dtype"] in (1, 2) else 4
     S = op["count"] * e * (1 if op["collective"] == "ALL_REDUCE" else world)
     if world > 1:

@@ -138,6 +138,9 @@ struct ReplayOptions {
   int nccl_reserve_sms = 0;
   // SIMPLE collectives move data with TMA bulk copies (lagom_comm_opts_t.use_tma).
   bool use_tma = true;
+  // Victim GEMMs run the fastest of cuBLASLt's top-8 heuristic algorithms
+  // for their shape and SM budget (timed once); false: the first candidate.
+  bool autotune_gemms = true;
   // PM sampling: metrics (empty = default_pm_metrics()) and interval.
   std::vector<std::string> pm_metrics;
   std::uint64_t pm_interval_ns = 20000;

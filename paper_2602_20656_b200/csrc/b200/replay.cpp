@@ -375,17 +375,6 @@ struct ReplayEngine::Impl {
                      "stride");
           }
         }
-        cublasLtMatmulPreference_t pref;
-        lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
-        lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
-                                                      &workspace_bytes, sizeof workspace_bytes),
-                 "pref ws");
-        cublasLtMatmulHeuristicResult_t res{};
-        int found = 0;
-        lt_check(cublasLtMatmulAlgoGetHeuristic(lt, g.desc, g.a, g.b, g.d, g.d, pref, 1, &res, &found), "heuristic");
-        cublasLtMatmulPreferenceDestroy(pref);
-        if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for GEMM shape");
-        g.algo = res.algo;
         // Operands are shared between GEMMs of identical shape (all layers of
         // a model): the values are synthetic and these GEMMs are compute-bound,
         // so sharing only bounds memory (a 32-layer DAG fits in HBM).
@@ -404,6 +393,7 @@ struct ReplayEngine::Impl {
         g.A = hit->second[0];
         g.B = hit->second[1];
         g.D = hit->second[2];
+        g.algo = fastest_algo(g, g.desc, 0);
         gemms[i].push_back(g);
       }
     }
@@ -538,6 +528,59 @@ struct ReplayEngine::Impl {
     }
   }
 
+  // The fastest of cuBLASLt's top heuristic candidates for this shape and SM
+  // target, timed here once (cached per shape and target). Every arm —
+  // isolated compute, NCCL, Lagom with or without the SM partition — thus
+  // runs the best GEMM kernel cuBLASLt has for its SM budget, so no arm gains
+  // or loses from a heuristic's mispick (the first candidate is not always
+  // the fastest on sm_100: e.g. Mixtral's expert GEMMs ran faster under an
+  // SM count target than at the full GPU with the first candidate).
+  std::map<std::tuple<std::int64_t, std::int64_t, std::int64_t, std::int64_t, int>, cublasLtMatmulAlgo_t> algo_cache;
+  cublasLtMatmulAlgo_t fastest_algo(Gemm& g, cublasLtMatmulDesc_t desc, int sm_target) {
+    const auto key = std::make_tuple(g.shape.m, g.shape.n, g.shape.k, g.shape.batch, sm_target);
+    if (auto it = algo_cache.find(key); it != algo_cache.end()) return it->second;
+    cublasLtMatmulPreference_t pref;
+    lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
+    lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &workspace_bytes,
+                                                  sizeof workspace_bytes),
+             "pref ws");
+    constexpr int kCands = 8;
+    cublasLtMatmulHeuristicResult_t res[kCands]{};
+    int found = 0;
+    lt_check(cublasLtMatmulAlgoGetHeuristic(lt, desc, g.a, g.b, g.d, g.d, pref, kCands, res, &found), "heuristic");
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for the GEMM shape");
+    int best = 0;
+    if (found > 1 && opts.autotune_gemms) {
+      cudaEvent_t e0, e1;
+      cuda_check(cudaEventCreate(&e0), "event");
+      cuda_check(cudaEventCreate(&e1), "event");
+      float best_ms = 1e30f;
+      const float alpha = 1.0f, beta = 0.0f;
+      for (int c = 0; c < found; ++c) {
+        if (res[c].state != CUBLAS_STATUS_SUCCESS) continue;
+        auto run = [&] {
+          return cublasLtMatmul(lt, desc, &alpha, g.A, g.a, g.B, g.b, &beta, g.D, g.d, g.D, g.d, &res[c].algo,
+                                workspace, workspace_bytes, cs);
+        };
+        if (run() != CUBLAS_STATUS_SUCCESS) continue;  // warm-up (and skip algos that refuse)
+        cuda_check(cudaEventRecord(e0, cs), "record");
+        for (int r = 0; r < 5; ++r) lt_check(run(), "cublasLtMatmul (autotune)");
+        cuda_check(cudaEventRecord(e1, cs), "record");
+        cuda_check(cudaEventSynchronize(e1), "sync");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+        if (ms < best_ms) {
+          best_ms = ms;
+          best = c;
+        }
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    return algo_cache.emplace(key, res[best].algo).first->second;
+  }
+
   // A plan for `sm_target` SMs (0 = the whole GPU): the SM partition that
   // leaves the collective's NC channels their own SMs (the contention
   // model's lambda - NC). Cached per target.
@@ -552,17 +595,7 @@ struct ReplayEngine::Impl {
     const int32_t target = sm_target;
     lt_check(cublasLtMatmulDescSetAttribute(p.desc, CUBLASLT_MATMUL_DESC_SM_COUNT_TARGET, &target, sizeof target),
              "sm target");
-    cublasLtMatmulPreference_t pref;
-    lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
-    lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &workspace_bytes,
-                                                  sizeof workspace_bytes),
-             "pref ws");
-    cublasLtMatmulHeuristicResult_t res{};
-    int found = 0;
-    lt_check(cublasLtMatmulAlgoGetHeuristic(lt, p.desc, g.a, g.b, g.d, g.d, pref, 1, &res, &found), "heuristic");
-    cublasLtMatmulPreferenceDestroy(pref);
-    if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for the SM target");
-    p.algo = res.algo;
+    p.algo = fastest_algo(g, p.desc, sm_target);
     return g.by_sm_target.emplace(sm_target, p).first->second;
   }
 
@@ -666,6 +699,12 @@ struct ReplayEngine::Impl {
       for (std::size_t i = 0; i < M; ++i)
         if (reserve[i] > 0) sm_target[i] = std::max(1, num_sms - reserve[i]);
     }
+    // Plans for new SM targets are built (and their algorithms timed) here,
+    // before the barrier and the start event — never inside the measurement.
+    if (do_compute)
+      for (std::size_t i = 0; i < M; ++i)
+        if (sm_target[i] > 0)
+          for (Gemm& g : gemms[i]) plan_for(g, sm_target[i]);
     coord.barrier();
     const bool e2e = mode == Mode::LagomE2E;
     cuda_check(cudaEventRecord(ev_start, cs), "record");

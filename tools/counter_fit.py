@@ -41,6 +41,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+from tools.contention_profile import predict as comm_predict  # noqa: E402
 from tools.predict_vs_measured import KIB, MIB, _builder, fit  # noqa: E402
 
 LAMBDA, WAVES = 148, 16
@@ -70,12 +71,14 @@ class Workload:
             e = 2 if c.get("dtype", 1) in (1, 2) else 4
             self.sizes.append(c["count"] * e * (1 if c["collective"] == "ALL_REDUCE" else self.n))
 
-    def work(self, gpu, bw):
+    def work(self, gpu, bw, y_iso=None):
+        """The reference Workload; y_iso (optional) overrides the isolated
+        compute times (a bench run's own compute-only replays)."""
         comps = []
         for i, c in enumerate(self.dag["compute_ops"]):
             co = self.prof["compute_ops"][i]
             d = co["dram_bytes"] / (LAMBDA * WAVES)
-            f = co["y_us"] / WAVES
+            f = (y_iso[i] if y_iso is not None else co["y_us"]) / WAVES
             comps.append({"id": c["id"], "total_blocks": LAMBDA * WAVES, "blocks_per_sm": 1,
                           "bytes_per_block": int(round(d)),
                           "base_wave_time": max(1e-3, f - LAMBDA * round(d) / bw)})
@@ -90,20 +93,48 @@ class Workload:
         return w
 
 
-def fit_params(wls):
+COLLS = ("ALL_REDUCE", "ALL_GATHER", "REDUCE_SCATTER", "ALL_TO_ALL")
+
+
+def fit_params(wls, extra=()):
+    """comm_time per subspace on its AllReduce points (or its most measured
+    collective), then the reference's collective_factors
+    (default_params.json:164-169) — one message-size factor per collective —
+    by 1-D search against those coefficients (median relative error).
+    extra: (key, collective, nc, nt, c, bytes, x) comm-alone points measured
+    elsewhere (the bench runs' comm-only replays at the tuned picks)."""
     by_key = {}
+    for key, coll, *pt in extra:
+        by_key.setdefault(key, {}).setdefault(coll, []).append(tuple(pt))
     for wl in wls:
         for st in wl.prof["sets"].values():
             cfg = st["config"]
             for j, co in enumerate(st["comm_ops"]):
-                f = 2.0 if wl.dag["comm_ops"][j]["collective"] == "ALL_REDUCE" else 1.0
-                by_key.setdefault(key_of(cfg), []).append(
-                    (cfg["num_channels"], cfg["num_threads"], cfg["chunk_size"], wl.sizes[j] * f, co["x_us"]))
+                by_key.setdefault(key_of(cfg), {}).setdefault(wl.dag["comm_ops"][j]["collective"], []).append(
+                    (cfg["num_channels"], cfg["num_threads"], cfg["chunk_size"], wl.sizes[j], co["x_us"]))
     params, report, links = {}, {}, {}
-    for key, pts in by_key.items():
-        co, lk, rep = fit(pts)
+    factors = {"ALL_REDUCE": 2.0}
+    main_key = max(by_key, key=lambda k: sum(len(v) for v in by_key[k].values()))
+    for key, colls in by_key.items():
+        base = "ALL_REDUCE" if "ALL_REDUCE" in colls else max(colls, key=lambda c: len(colls[c]))
+        bf = 2.0 if base == "ALL_REDUCE" else 1.0
+        co, lk, rep = fit([(nc, nt, c, m * bf, x) for nc, nt, c, m, x in colls[base]])
         params[key], links[key] = co, lk
-        report[key] = dict(rep, link_bw=lk)
+        report[key] = dict(rep, link_bw=lk, base_collective=base)
+        if key != main_key:
+            continue
+        factors[base] = bf
+        for coll, pts in colls.items():
+            if coll == base:
+                continue
+            best = None
+            for f in np.geomspace(0.1, 10.0, 241):
+                rel = [abs(comm_predict(co, lk, nc, nt, c, m * f) - x) / x for nc, nt, c, m, x in pts]
+                err = float(np.median(rel))
+                if best is None or err < best[0]:
+                    best = (err, float(f))
+            factors[coll] = best[1]
+            report[key][f"factor_{coll}"] = {"factor": best[1], "median_rel_err": best[0], "points": len(pts)}
     for key in by_key:  # footprint V: HBM bytes per us of comm, per set
         vpts = []
         for wl in wls:
@@ -128,19 +159,19 @@ def fit_params(wls):
     for key in ("RING/SIMPLE/P2P", "RING/LL/P2P", "RING/LL128/P2P", "TREE/SIMPLE/P2P", "TREE/LL/P2P",
                 "TREE/LL128/P2P"):
         params.setdefault(key, dict(base))
-    params["collective_factors"] = {"ALL_REDUCE": 2.0, "ALL_GATHER": 1.0, "REDUCE_SCATTER": 1.0, "ALL_TO_ALL": 1.0}
+    params["collective_factors"] = {c: factors.get(c, 1.0) for c in COLLS}
     return params, report, links
 
 
-def predict(wl, cfgs, params, links, g, nvls):
+def predict(wl, cfgs, params, links, g, nvls, y_iso=None):
     from paper_2602_20656_b200 import _lagom_py as L
     co = all(coresident(c, nvls) for c in cfgs)
     key = key_of(cfgs[0])
     bw = g["B_co"] if co else g["B"]
     gpu = {"num_sms": LAMBDA, "link_bw": links.get(key, next(iter(links.values()))), "comm_bw_cap_fraction": 0.6,
            "compute_on_comm_slowdown": g["delta_co"] if co else g["delta_ded"]}
-    sim = json.loads(L.simulate(json.dumps(wl.work(gpu, bw)), json.dumps({"configs": cfgs}), json.dumps(params),
-                                not co))
+    sim = json.loads(L.simulate(json.dumps(wl.work(gpu, bw, y_iso)), json.dumps({"configs": cfgs}),
+                                json.dumps(params), not co))
     return sim, co
 
 
@@ -153,7 +184,26 @@ def main():
     a = ap.parse_args()
     profs = [json.load(open(p)) for f in a.profiles for p in sorted(glob.glob(f))]
     wls = [Workload(p) for p in profs if p["n"] == a.n]
-    params, report, links = fit_params(wls)
+    benches = []
+    for f in a.bench:
+        for p in sorted(glob.glob(f)):
+            if p.endswith("_lagom.json") or p.endswith("_nccl.json"):
+                continue
+            b = json.load(open(p))
+            if b["line"]["n_gpus"] == a.n:
+                benches.append(b)
+    # the bench runs' comm-only replays at the tuned picks join the comm fit
+    extra = []
+    for b in benches:
+        wl = next((w for w in wls if w.prof["workload"] == b["line"]["config"]["workload"]), None)
+        if wl is None:
+            continue
+        cfgs = [b["tune"]["configs"][gi] for gi in _groups(wl.dag)]
+        xs = np.median([r["x"] for r in b["raw"]["comm"]], axis=0)
+        for j, cfg in enumerate(cfgs):
+            extra.append((key_of(cfg), wl.dag["comm_ops"][j]["collective"], cfg["num_channels"], cfg["num_threads"],
+                          cfg["chunk_size"], wl.sizes[j], float(xs[j])))
+    params, report, links = fit_params(wls, extra)
     B = hbm_peak()
     sets = [(wl, spec, st) for wl in wls for spec, st in wl.prof["sets"].items()]
 
@@ -182,25 +232,21 @@ def main():
                      "Z_pred": sim["Z"], "Z_meas": m["Z"], "Z_err": (sim["Z"] - m["Z"]) / m["Z"],
                      "Y_err": (sim["Y"] - m["Y"]) / m["Y"]})
     bench_rows = []
-    for f in a.bench:
-        for p in sorted(glob.glob(f)):
-            if p.endswith("_lagom.json") or p.endswith("_nccl.json"):
-                continue
-            b = json.load(open(p))
-            line = b["line"]
-            if line["n_gpus"] != a.n:
-                continue
-            wname = line["config"]["workload"]
-            wl = next((w for w in wls if w.prof["workload"] == wname), None)
-            if wl is None:
-                continue
-            groups = _groups(wl.dag)
-            cfgs = [b["tune"]["configs"][gi] for gi in groups]
-            nvls = line["lagom"]["nvls"]["active"]
-            sim, co = predict(wl, cfgs, params, links, g, nvls)
-            meas = line["arms_ms"]["lagom"] * 1e3
-            bench_rows.append({"workload": wname, "n": a.n, "picks": sorted(set(line["lagom"]["tune"]["picks"])),
-                               "coresident": co, "Z_pred": sim["Z"], "Z_meas": meas, "Z_err": (sim["Z"] - meas) / meas})
+    for b in benches:
+        line = b["line"]
+        wname = line["config"]["workload"]
+        wl = next((w for w in wls if w.prof["workload"] == wname), None)
+        if wl is None:
+            continue
+        cfgs = [b["tune"]["configs"][gi] for gi in _groups(wl.dag)]
+        nvls = line["lagom"]["nvls"]["active"]
+        # isolated compute times from the bench run's own interleaved compute-only arm
+        y_iso = [float(v) for v in np.median([r["y"] for r in b["raw"]["compute"]], axis=0)]
+        sim, co = predict(wl, cfgs, params, links, g, nvls, y_iso)
+        meas = line["arms_ms"]["lagom"] * 1e3
+        bench_rows.append({"workload": wname, "n": a.n, "picks": sorted(set(line["lagom"]["tune"]["picks"])),
+                           "coresident": co, "Z_pred": sim["Z"], "Z_meas": meas, "Z_err": (sim["Z"] - meas) / meas,
+                           "Y_pred": sim["Y"], "Y_meas": line["compute"]["overlapped_ms"] * 1e3})
     res = {"n": a.n, "global": g, "fit_score_median_abs_Z_err": best[0], "params": params, "fit_report": report,
            "sets": rows, "bench_rows": bench_rows,
            "note": "sets: the profile's own overlapped replays (every comm op at one config); bench_rows: bench.py's "
