@@ -252,6 +252,7 @@ struct ReplayEngine::Impl {
   void* host_out = nullptr;  // pinned
   int calls = 0;
   bool pm_on = false;
+  std::vector<std::int64_t> model_blocks;  // per compute op: the CTAs to_workload models (trace args.blocks)
   std::unique_ptr<PmSampler> sampler;  // created on first use (each rank, its own GPU)
   unsigned long long* stamp = nullptr;  // device: %globaltimer at the replay start
   bool nvls_on = false;
@@ -269,6 +270,7 @@ struct ReplayEngine::Impl {
     cuda_check(cudaMalloc(&workspace, workspace_bytes), "workspace");
     build_gemms();
     build_attention();
+    for (const ComputeOp& op : to_workload(dag, GpuSpec{}, n).compute_ops) model_blocks.push_back(op.total_blocks);
     build_comm_backends();
     build_comms();
     auto mk = [](cudaEvent_t* e) { cuda_check(cudaEventCreate(e), "event"); };
@@ -774,7 +776,7 @@ struct ReplayEngine::Impl {
     if (do_compute)
       for (std::size_t i = 0; i < M; ++i)
         last_timeline.push_back({"compute", dag.compute_ops[i].id, us(ev_start, ev_cb[i]), out[N + i],
-                                 static_cast<std::int64_t>(gemms[i].size())});
+                                 model_blocks[i]});
     if (do_comm)
       for (std::size_t j = 0; j < N; ++j)
         last_timeline.push_back({"comm", dag.comm_ops[j].id, us(ev_start, ev_kb[j]), out[j], 0});
