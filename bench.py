@@ -293,6 +293,7 @@ def main():
                     help="NVLS / one-hop / single-rank kernels sized to co-reside with GEMM CTAs")
     ap.add_argument("--one-hop", type=int, default=0,
                     help="lagom_comm_opts_t.one_hop: TREE AG/RS through the switch (0), one hop (1), one hop at n = 2 (2)")
+    ap.add_argument("--a2a-tma", type=int, default=0, help="lagom_comm_opts_t.a2a_tma (one-hop AllToAll via TMA)")
     ap.add_argument("--ablations", type=int, default=1,
                     help="also time: our kernels at the seed with the SM partition forced on, and (N > 1) NCCL "
                          "with the GEMMs on num_sms - NCCL's channels")
@@ -346,7 +347,8 @@ def main():
     eng = L.ReplayEngine(json.dumps(dag), f"lagom_{token}", rank, world, local, repeats=1, warmup=0,
                          nccl=not args.no_nccl, e2e_in_bytes=T_in_bytes, e2e_out_bytes=4096,
                          sm_partition=args.sm_partition, max_channels=max(32, args.nc_max),
-                         nvls=bool(args.nvls), coresident=bool(args.coresident), one_hop=args.one_hop)
+                         nvls=bool(args.nvls), coresident=bool(args.coresident), one_hop=args.one_hop,
+                         a2a_tma=bool(args.a2a_tma))
     nvls_state = {"requested": bool(args.nvls) and world > 1, "active": bool(eng.nvls_active),
                   "peer_mappings": bool(eng.nvls_peers_active)}
     result, tuned, tune_wall_s, tune_runs = None, None, 0.0, {}

@@ -1,6 +1,9 @@
-"""Prints DESIGN.md §6's result tables from the committed bench lines and
-predicted-vs-measured files (profiles/round1_final_n{1,2,4}_*.json,
-profiles/round1_predict_vs_measured_n{2,4}_*.json). No GPU."""
+"""Prints DESIGN.md §6's result tables from the committed round-2 files:
+bench lines (profiles/round2_final_n{N}_{workload}.json) and the
+counter-backed model (profiles/round2_model_n{N}.json). No GPU.
+
+  python tools/results_tables.py
+"""
 import json
 import os
 
@@ -9,45 +12,76 @@ NAMES = {"gpt2-1.3b-dp": "GPT-2 1.3B DP (2)", "llama3-8b-tp-sp": "Llama-3 8B TP-
          "llama3-70b-fsdp": "Llama-3 70B-layer FSDP (4)", "mixtral-8x7b-ep": "Mixtral 8x7B EP (5)"}
 
 
-def prof(name):
-    return json.load(open(os.path.join(ROOT, "profiles", name)))
+def load(name):
+    p = os.path.join(ROOT, "profiles", name)
+    return json.load(open(p)) if os.path.exists(p) else None
+
+
+def picks(line):
+    ps = sorted(set(line["lagom"]["tune"]["picks"]))
+    ncs = sorted({int(p.split("/NC")[1].split("/")[0]) for p in ps})
+    nts = sorted({int(p.split("/NT")[1].split("/")[0]) for p in ps})
+    nc = f"NC{ncs[0]}" if len(ncs) == 1 else f"NC{ncs[0]}–{ncs[-1]}"
+    nt = f"NT{nts[0]}" if len(nts) == 1 else f"NT{nts[0]}–{nts[-1]}"
+    return f"{ps[0].split('/')[0]} {nc} {nt}"
+
+
+def fmt(v, nd=2):
+    return "—" if v is None else f"{v:.{nd}f}"
 
 
 def bench_rows():
-    out = ["| workload (BASELINE config) | N | Lagom-tuned | NCCL-default | speedup | Lagom picks | "
-           "compute slowdown (Lagom / NCCL) | roofline frac |", "|---|---|---|---|---|---|---|---|"]
-    for n in (4, 2):
+    out = ["| workload (BASELINE config) | N | Lagom-tuned | NCCL-default | speedup | ours @ seed | "
+           "ours @ seed + SM partition | NCCL + SM partition | compute only | picks | compute slowdown "
+           "(Lagom / NCCL) | roofline frac (wire) |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    for n in (4, 2, 1):
         for w, name in NAMES.items():
-            l = prof(f"round1_final_n{n}_{w}.json")["line"]
-            c = l["compute"]
-            ncs = sorted({int(p.split("/NC")[1].split("/")[0]) for p in l["config"]["tune"]["picks"]})
-            nc = f"NC{ncs[0]}" if len(ncs) == 1 else f"NC{ncs[0]}–{ncs[-1]}"
-            kind = "A2A one-hop" if w.startswith("mixtral") else "NVLS"
-            sp = l["speedup_vs_nccl_default"]
-            sps = f"**{sp:.3f}×**" if sp >= 1.07 else f"{sp:.3f}×"
-            out.append(f"| {name} | {n} | {l['value']:.2f} | {l['nccl_default_ms']:.2f} | {sps} | TREE ({kind}) {nc} | "
-                       f"{c['slowdown']:.3f} / {c['slowdown_nccl']:.3f} | {l['roofline']['frac']:.3f} |")
-    l = prof("round1_final_n1_gpt2-1.3b-dp.json")["line"]
-    c = l["compute"]
-    out.append(f"| GPT-2 1.3B DP (2) | 1 | {l['value']:.2f} | {l['nccl_default_ms']:.2f} | "
-               f"{l['speedup_vs_nccl_default']:.3f}× | copy NC8/NT512 | {c['slowdown']:.3f} / {c['slowdown_nccl']:.3f} | "
-               f"{l['roofline']['frac']:.3f} (HBM; 8 of 148 SMs) |")
+            d = load(f"round2_final_n{n}_{w}.json")
+            if not d:
+                continue
+            line = d["line"]
+            a, c = line["arms_ms"], line["compute"]
+            sp = line["speedup_vs_nccl_default"]
+            sps = f"**{sp:.3f}×**" if sp and sp >= 1.07 else f"{sp:.3f}×"
+            out.append(f"| {name} | {n} | {a['lagom']:.2f} | {fmt(a.get('nccl'))} | {sps} | {fmt(a.get('seed'))} | "
+                       f"{fmt(a.get('seed_partition_all'))} | {fmt(a.get('nccl_partition'))} | {a['compute']:.2f} | "
+                       f"{picks(line)} | {c['slowdown']:.3f} / {fmt(c.get('slowdown_nccl'), 3)} | "
+                       f"{line['roofline']['frac']:.3f} |")
     return "\n".join(out)
 
 
-def pvm_rows():
-    out = ["| workload | N | predicted Z (ms) | measured Z (ms) | Z error | Y error | X error |",
-           "|---|---|---|---|---|---|---|"]
+def model_rows():
+    out = ["| workload | N | picks | predicted Z (ms) | measured Z (ms) | error |", "|---|---|---|---|---|---|"]
     for n in (4, 2):
-        for w, name in NAMES.items():
-            p = prof(f"round1_predict_vs_measured_n{n}_{w}.json")
-            e = p["rel_err"]
-            out.append(f"| {name} | {n} | {p['predicted']['Z'] / 1e3:.2f} | {p['measured']['Z'] / 1e3:.2f} | "
-                       f"{e['Z'] * 100:+.1f} % | {e['Y'] * 100:+.1f} % | {e['X'] * 100:+.1f} % |")
+        m = load(f"round2_model_n{n}.json")
+        if not m:
+            continue
+        for r in m["bench_rows"]:
+            w = next((k for k in NAMES if r["workload"].startswith(k.split("-")[0] + "-" + k.split("-")[1])),
+                     r["workload"])
+            out.append(f"| {NAMES.get(w, r['workload'])} | {n} | {len(r['picks'])} configs | {r['Z_pred'] / 1e3:.2f} | "
+                       f"{r['Z_meas'] / 1e3:.2f} | {r['Z_err'] * 100:+.1f} % |")
+    return "\n".join(out)
+
+
+def model_set_summary():
+    out = ["| N | sets | median abs Z error | within 5 % | delta (dedicated / co-resident) |", "|---|---|---|---|---|"]
+    for n in (4, 2):
+        m = load(f"round2_model_n{n}.json")
+        if not m:
+            continue
+        errs = sorted(abs(r["Z_err"]) for r in m["sets"])
+        within = sum(e <= 0.05 for e in errs)
+        g = m["global"]
+        out.append(f"| {n} | {len(errs)} | {errs[len(errs) // 2] * 100:.1f} % | {within} / {len(errs)} | "
+                   f"{g['delta_ded']} / {g['delta_co']} |")
     return "\n".join(out)
 
 
 if __name__ == "__main__":
     print(bench_rows())
     print()
-    print(pvm_rows())
+    print(model_rows())
+    print()
+    print(model_set_summary())
