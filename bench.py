@@ -278,8 +278,10 @@ def main():
     ap.add_argument("--impl", default="lagom", choices=["lagom", "reference"])
     ap.add_argument("--workload", default="gpt2-1.3b-dp")
     ap.add_argument("--budget", type=int, default=120)
-    ap.add_argument("--start", default="best", choices=["min", "nccl-default", "best"],
-                    help="tune() seed (reference CLI --start); best = run both, keep the lower final Z")
+    ap.add_argument("--start", default="best", choices=["min", "nccl-default", "coresident", "best"],
+                    help="tune() seed: the reference CLI's min / nccl-default, or coresident (NC 64, NT 128: "
+                         "the co-resident kernel regime); best = run all three, keep the lowest final Z "
+                         "(head to head)")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--nc-max", type=int, default=64, help="per-op CommBounds.nc_max for the search")
     ap.add_argument("--nvls", type=int, default=1, help="comm buffers in an NVLS region (TREE = in-switch)")
@@ -360,7 +362,7 @@ def main():
         # (k-th bucket of every layer) share one config.
         t_tune = time.perf_counter()
         eng.run_compute_only()  # first-touch / clocks settle before the search
-        starts = ["min", "nccl-default"] if args.start == "best" else [args.start]
+        starts = ["min", "nccl-default", "coresident"] if args.start == "best" else [args.start]
         eng.set_partition(args.sm_partition, 0)
         eng.set_measurement(5, 2)  # each profile call: median of 5 replays after 2 warmups
         params_doc = open(args.params).read() if args.params and os.path.exists(args.params) else ""
@@ -375,8 +377,11 @@ def main():
         docs = {st: json.dumps({"configs": [r["configs"][g] for g in groups]}) for st, r in runs.items()}
         zsel = {st: [] for st in runs}
         order = list(runs)
-        for i in range(6 if len(runs) > 1 else 0):  # alternating order, so neither keeps a predecessor
-            for st in (order if i % 2 == 0 else order[::-1]):
+        sel_rng = random.Random(args.order_seed + 1)
+        for i in range(6 if len(runs) > 1 else 0):  # random order per round: no start keeps a predecessor
+            perm = order[:]
+            sel_rng.shuffle(perm)
+            for st in perm:
                 zsel[st].append(json.loads(eng.run(docs[st]))["Z"])
         best_start = min(runs, key=lambda st: statistics.median(zsel[st]) if zsel[st] else 0.0)
         tune_runs = runs

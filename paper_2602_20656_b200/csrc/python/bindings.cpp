@@ -42,8 +42,13 @@ Json profile_json(const ProfileResult& p) {
 // Reference CLI seeds (lagom_main.cpp:181-198): min or nccl-default.
 std::vector<CommConfig> seed_configs(const Workload& w, const SubspaceParams& params,
                                      const std::string& start) {
-  if (start != "min" && start != "nccl-default")
-    throw Error(ErrorCode::InvalidInput, "start", "expected min|nccl-default");
+  // min / nccl-default: the reference CLI's starts (lagom_main.cpp --start).
+  // coresident (B200 addition): many light channels that ride along the
+  // GEMMs (NC 64, NT 128 — the co-resident kernel regime of the NVLS, one-hop
+  // and single-rank kernels, lagom_coll.h), a region neither reference start
+  // reaches, since Alg. 2 only grows resources (tuner.cpp:47-76).
+  if (start != "min" && start != "nccl-default" && start != "coresident")
+    throw Error(ErrorCode::InvalidInput, "start", "expected min|nccl-default|coresident");
   std::vector<CommConfig> out;
   for (const CommOp& op : w.comm_ops) {
     const StepBounds b = bounds_for(op, w.gpu);
@@ -51,6 +56,10 @@ std::vector<CommConfig> seed_configs(const Workload& w, const SubspaceParams& pa
     if (start == "nccl-default") {
       c.num_channels = std::min(8, b.nc_max);
       c.num_threads = 512;
+      c.chunk_size = std::clamp<std::int64_t>(2048 * kKiB, b.c_min, b.c_max);
+    } else if (start == "coresident") {
+      c.num_channels = std::min(64, b.nc_max);
+      c.num_threads = 128;
       c.chunk_size = std::clamp<std::int64_t>(2048 * kKiB, b.c_min, b.c_max);
     }
     out.push_back(c);
