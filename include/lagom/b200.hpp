@@ -148,7 +148,7 @@ struct ReplayOptions {
   // same on every rank).
   bool coresident = true;
   int one_hop = 0;
-  bool a2a_tma = false;
+  bool a2a_tma = true;
   // NVSwitch multicast: comm buffers live in an NVLS region, so TREE
   // AllReduce/AllGather/ReduceScatter run reduced/broadcast in the switch.
   bool nvls = false;

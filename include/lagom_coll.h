@@ -77,8 +77,10 @@ typedef struct {
                               (AG: peer stores; RS: pushes into the owners' scratch, see
                               lagom_comm_nvls_scratch), 2 one hop at nranks == 2 (where
                               the multicast echo caps the switch schedules)           */
-  int a2a_tma;             /* one-hop AllToAll through the TMA engine (192 KB smem ring
-                              per CTA, cannot share an SM with a GEMM); default 0      */
+  int a2a_tma;             /* 1 (default): the one-hop AllToAll moves data with TMA bulk
+                              copies (one elected thread, 192 KB smem ring: the CTA takes
+                              an SM) except in the co-resident regime (coresident and NT
+                              <= 256), which keeps vector stores; 0: vector stores always */
 } lagom_comm_opts_t;
 
 typedef struct {

@@ -256,7 +256,7 @@ void lagom_comm_default_opts(lagom_comm_opts_t* o) {
   o->use_tma = 1;
   o->coresident = 1;
   o->one_hop = 0;
-  o->a2a_tma = 0;
+  o->a2a_tma = 1;
 }
 
 int lagom_comm_create(int rank, int nranks, int device, const lagom_comm_opts_t* opts,

@@ -615,7 +615,9 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
     case LAGOM_ALL_TO_ALL:
       if (!c->nvls_peers_ready) return 0;
       in_b = out_b = a->count * e * n;
-      if (c->opts.a2a_tma) {
+      // TMA bulk copies (one elected thread, 192 KB smem ring: an SM of its
+      // own) unless the config asks for the co-resident regime (NT <= 256)
+      if (c->opts.a2a_tma && !(co && a->num_threads <= 256)) {
         static const bool smem_ok =
             cudaFuncSetAttribute(reinterpret_cast<const void*>(&a2a_tma_kernel),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;

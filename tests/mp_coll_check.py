@@ -59,7 +59,7 @@ def main():
     comm = C.Communicator.from_process_group(device=local, max_channels=32, max_chunk_bytes=4 << 20,
                                              timeout_ms=5000, use_tma=use_tma,
                                              one_hop=int(os.environ.get("LAGOM_ONE_HOP", "0")),
-                                             a2a_tma=int(os.environ.get("LAGOM_A2A_TMA", "0")),
+                                             a2a_tma=int(os.environ.get("LAGOM_A2A_TMA", "1")),
                                              coresident=int(os.environ.get("LAGOM_CORESIDENT", "1")))
     stream = torch.cuda.current_stream().cuda_stream
     nvls = bool(os.environ.get("LAGOM_NVLS")) and comm.nvls_supported()

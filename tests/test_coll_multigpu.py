@@ -25,14 +25,15 @@ def _gpus():
         return 0
 
 
-@pytest.mark.parametrize("variant", ["p2p", "nvls", "nvls-deep", "nvls-a2a-tma"])
+@pytest.mark.parametrize("variant", ["p2p", "nvls", "nvls-deep", "nvls-a2a-lsu"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_real_multigpu_parity(world, variant):
     """nvls: buffers in a multicast region, so TREE AllReduce runs inside
     the NVSwitch (int32 and movement bit-exact; fp sums within the stated
     bound of the fp64 exact sum, since the switch accumulates in fp32 in its
     own order). nvls = the co-resident kernels (default), nvls-deep = the
-    deep-unroll ones (coresident = 0), nvls-a2a-tma = the TMA AllToAll."""
+    deep-unroll ones (coresident = 0), nvls-a2a-lsu = the vector-store AllToAll
+    at every NT (a2a_tma = 0; the default moves large-NT AllToAll with TMA)."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ)
@@ -40,8 +41,8 @@ def test_real_multigpu_parity(world, variant):
         env["LAGOM_NVLS"] = "1"
     if variant == "nvls-deep":
         env["LAGOM_CORESIDENT"] = "0"
-    if variant == "nvls-a2a-tma":
-        env["LAGOM_A2A_TMA"] = "1"
+    if variant == "nvls-a2a-lsu":
+        env["LAGOM_A2A_TMA"] = "0"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]
