@@ -104,3 +104,27 @@ def test_shm_coordinator_multiprocess(world):
             assert rec["msg"] == f"round-{k}-of-{world}"
             assert rec["gathered"] == [100 * q_ + k for q_ in range(world)]
             assert rec["max"] == [world - 1, 0.0, 1.5 * (world - 1) + k]
+
+
+def test_reference_arm_times_every_comm_op(root):
+    """bench.py --impl reference: the reference's CPU path (the CPU collective
+    restatement over every comm op of the iteration, prefaulted rotating
+    buffers) prints the bench line contract with the Lagom arm's metric,
+    unit and workload config, and a cpu_baseline describing the run."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    sys.path.insert(0, root)
+    import bench
+    from paper_2602_20656_b200 import dags
+    assert line["impl"] == "reference" and line["metric"] == bench.METRIC and line["unit"] == "ms"
+    assert line["config"] == bench.workload_config(dags.BUILDERS["gpt2-1.3b-dp"](1))
+    assert line["value"] > 0 and line["higher_is_better"] is False
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert "all 96 comm ops" in cb["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
