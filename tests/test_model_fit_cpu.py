@@ -57,3 +57,27 @@ def test_predicted_overlap_time_all_rows(tmp_path, fit_cache, n, workload):
     assert got["predicted"]["Z"] == pytest.approx(committed["predicted"]["Z"], rel=1e-12)
     assert got["rel_err"]["Z"] == pytest.approx(committed["rel_err"]["Z"], rel=1e-9)
     assert (abs(got["rel_err"]["Z"]) <= 0.05) == ((n, workload) not in OUT_OF_BOUND)
+
+
+ROUND2 = [n for n in (4, 2) if os.path.exists(os.path.join(ROOT, "profiles", f"round2_model_n{n}.json"))]
+
+
+@pytest.mark.parametrize("n", ROUND2)
+def test_counter_model_rows_reproduce(tmp_path, n):
+    """Round 2's counter-backed model (tools/counter_fit.py) re-derived from
+    the committed CUPTI counter profiles and bench lines with the committed
+    global parameters: every config set's and every bench row's predicted Z
+    is reproduced, so the errors DESIGN.md §7 states are the real ones —
+    inside and outside the 5 % bound alike."""
+    out = tmp_path / "model.json"
+    committed_path = os.path.join(ROOT, "profiles", f"round2_model_n{n}.json")
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "counter_fit.py"), "--n", str(n),
+                    "--profiles", os.path.join(ROOT, "profiles", f"round2_counters_n{n}_*.json"),
+                    "--bench", os.path.join(ROOT, "profiles", f"round2_final_n{n}_*.json"),
+                    "--globals", committed_path, "--out", str(out)], cwd=ROOT, check=True, capture_output=True,
+                   timeout=900)
+    got, committed = json.load(open(out)), json.load(open(committed_path))
+    assert len(got["sets"]) == len(committed["sets"]) and len(got["bench_rows"]) == len(committed["bench_rows"])
+    for a, b in zip(got["sets"] + got["bench_rows"], committed["sets"] + committed["bench_rows"]):
+        assert a["Z_pred"] == pytest.approx(b["Z_pred"], rel=1e-9)
+        assert a["Z_err"] == pytest.approx(b["Z_err"], rel=1e-9, abs=1e-12)

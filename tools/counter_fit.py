@@ -20,14 +20,16 @@ Calibration (no GPU; every input is a measurement in the files):
               = lambda x waves; theta matches the isolated time at V = 0;
   regime      a set whose kernels ride along the GEMMs (co-resident: TREE with
               NT <= 256 on NVLS) holds no SMs (SimOptions.sm_occupancy =
-              false) but shares each SM's memory pipe: the model's bandwidth
-              B for those sets is a fitted B_co (reference wave_time's
-              peak_mem_bw - V, with D and theta refitted so the isolated time
-              is unchanged); dedicated sets keep B = measured HBM peak and
-              lose their NC SMs (sm_occupancy = true);
+              false); dedicated sets lose their NC SMs (sm_occupancy = true);
+              each regime's bandwidth B (reference wave_time's peak_mem_bw -
+              V, with theta refitted so the isolated time is unchanged) is
+              fitted;
   delta       compute_on_comm_slowdown, one per regime;
-three global parameters (delta_dedicated, delta_coresident, B_co) fitted by
-grid search over all sets of all workloads (median |Z error|).
+four global parameters (delta and the effective bandwidth B of each regime)
+fitted by grid search over all sets of all workloads (median |Z error|): the
+bandwidth the overlapped victims see is below the HBM copy peak once the
+collective's traffic shares the L2 and the SMs' memory pipes, and the fit
+states how far.
 """
 import argparse
 import glob
@@ -167,7 +169,7 @@ def predict(wl, cfgs, params, links, g, nvls, y_iso=None):
     from paper_2602_20656_b200 import _lagom_py as L
     co = all(coresident(c, nvls) for c in cfgs)
     key = key_of(cfgs[0])
-    bw = g["B_co"] if co else g["B"]
+    bw = g["B_co"] if co else g["B_ded"]
     gpu = {"num_sms": LAMBDA, "link_bw": links.get(key, next(iter(links.values()))), "comm_bw_cap_fraction": 0.6,
            "compute_on_comm_slowdown": g["delta_co"] if co else g["delta_ded"]}
     sim = json.loads(L.simulate(json.dumps(wl.work(gpu, bw, y_iso)), json.dumps({"configs": cfgs}),
@@ -181,6 +183,8 @@ def main():
     ap.add_argument("--profiles", nargs="+", required=True)
     ap.add_argument("--bench", nargs="*", default=[])
     ap.add_argument("--out", default="")
+    ap.add_argument("--globals", default="", help="take the four global parameters from this model file "
+                    "instead of the grid search (re-derives its rows; tests/test_model_fit_cpu.py)")
     a = ap.parse_args()
     profs = [json.load(open(p)) for f in a.profiles for p in sorted(glob.glob(f))]
     wls = [Workload(p) for p in profs if p["n"] == a.n]
@@ -215,14 +219,19 @@ def main():
         return out
 
     best = None
-    for dd in (0.0, 0.05, 0.1, 0.2, 0.3, 0.5):
+    fractions = (1.0, 1 / 1.5, 1 / 2, 1 / 3, 1 / 4, 1 / 6)
+    if a.globals:
+        g0 = json.load(open(a.globals))["global"]
+        best = (float(np.median(np.abs(errors(g0)))), g0)
+    for dd in (() if a.globals else (0.0, 0.1, 0.2, 0.3, 0.5)):
         for dc in (0.0, 0.1, 0.2, 0.3, 0.5, 0.8):
-            for bco in (B, B / 2, B / 3, B / 4, B / 6, B / 8):
-                g = {"B": B, "B_co": bco, "delta_ded": dd, "delta_co": dc}
-                e = errors(g)
-                score = float(np.median(np.abs(e)))
-                if best is None or score < best[0]:
-                    best = (score, g)
+            for fd in fractions:
+                for fc in fractions:
+                    g = {"B": B, "B_ded": B * fd, "B_co": B * fc, "delta_ded": dd, "delta_co": dc}
+                    e = errors(g)
+                    score = float(np.median(np.abs(e)))
+                    if best is None or score < best[0]:
+                        best = (score, g)
     g = best[1]
     rows = []
     for wl, spec, st in sets:
