@@ -457,14 +457,16 @@ def main():
     ms_nccl = ms.get("nccl")
     y_iso = y["compute"]
 
-    # dominant kernel: the comm op with the largest summed x over the DAG,
-    # timed alone at its tuned config (comm-only replay)
+    # dominant kernel: the config group (comm ops sharing one tuned config)
+    # with the largest summed x over the DAG; its first op, timed alone at the
+    # tuned config (comm-only replay), is the roofline's launch
     import collections
     x_sum = collections.defaultdict(float)
     for r in result["lagom"]:
         for j, x in enumerate(r["x"]):
-            x_sum[j] += x
-    j_dom = max(x_sum, key=x_sum.get) if x_sum else 0
+            x_sum[groups[j]] += x
+    g_dom = max(x_sum, key=x_sum.get) if x_sum else 0
+    j_dom = groups.index(g_dom)
     op = dag["comm_ops"][j_dom]
     cfg_dom = full_cfgs[j_dom]
     t_ev = statistics.median(r["x_ev"][j_dom] for r in result["comm"])    # CUDA events, us
