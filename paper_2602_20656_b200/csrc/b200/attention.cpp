@@ -9,6 +9,7 @@
 #include <cudnn.h>
 #include <cudnn_frontend.h>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -35,17 +36,19 @@ enum Uid : int64_t { kQ = 1, kK, kV, kO, kStats, kdO, kdQ, kdK, kdV };
 
 struct Attention::Impl {
   AttentionShape shape;
-  std::shared_ptr<fe::graph::Graph> graph;
+  std::unordered_map<int, std::shared_ptr<fe::graph::Graph>> graphs;  // per SM count target (0 = all)
   std::unordered_map<int64_t, void*> ptrs;
   std::vector<void*> owned;
   int64_t workspace = 0;
+  void build(cudnnHandle_t handle, int sm_target);
 };
 
-Attention::Attention(const AttentionShape& s, void* cudnn_handle, std::uint64_t seed, void* stream)
-    : impl_(std::make_unique<Impl>()) {
-  Impl& I = *impl_;
-  I.shape = s;
-  auto* handle = static_cast<cudnnHandle_t>(cudnn_handle);
+// One cuDNN graph and plan per SM count target: the replay's SM partition
+// restricts the attention victims like the GEMMs (the graph's sm_count knob,
+// CUDNN_ATTR_ENGINE_SM_COUNT_TARGET), so a dedicated collective's SMs are
+// not taken by the attention's CTAs either.
+void Attention::Impl::build(cudnnHandle_t handle, int sm_target) {
+  const AttentionShape& s = shape;
   const int64_t b = s.batch, h = s.heads, n = s.seq, d = s.head_dim;
   const std::vector<int64_t> dim{b, h, n, d}, stride{h * n * d, n * d, d, 1};
   const std::vector<int64_t> sdim{b, h, n, 1}, sstride{h * n, n, 1, 1};
@@ -53,6 +56,7 @@ Attention::Attention(const AttentionShape& s, void* cudnn_handle, std::uint64_t 
   g->set_io_data_type(fe::DataType_t::BFLOAT16)
       .set_intermediate_data_type(fe::DataType_t::FLOAT)
       .set_compute_data_type(fe::DataType_t::FLOAT);
+  if (sm_target > 0) g->set_sm_count(sm_target);
   auto tensor = [&](const char* name, int64_t uid) {
     return g->tensor(fe::graph::Tensor_attributes().set_name(name).set_dim(dim).set_stride(stride).set_uid(uid));
   };
@@ -80,8 +84,18 @@ Attention::Attention(const AttentionShape& s, void* cudnn_handle, std::uint64_t 
   fe_check(g->create_execution_plans({fe::HeurMode_t::A}), "create_execution_plans");
   fe_check(g->check_support(handle), "check_support");
   fe_check(g->build_plans(handle), "build_plans");
-  fe_check(g->get_workspace_size(I.workspace), "workspace size");
-  I.graph = g;
+  int64_t ws = 0;
+  fe_check(g->get_workspace_size(ws), "workspace size");
+  workspace = std::max(workspace, ws);
+  graphs[sm_target] = g;
+}
+
+Attention::Attention(const AttentionShape& s, void* cudnn_handle, std::uint64_t seed, void* stream)
+    : impl_(std::make_unique<Impl>()) {
+  Impl& I = *impl_;
+  I.shape = s;
+  const int64_t b = s.batch, h = s.heads, n = s.seq, d = s.head_dim;
+  I.build(static_cast<cudnnHandle_t>(cudnn_handle), 0);
   // device tensors: bf16 operands filled with N-like synthetic data, fp32 stats
   const int64_t elems = b * h * n * d;
   auto alloc = [&](int64_t uid, int64_t bytes, bool fill, int dtype) {
@@ -110,11 +124,17 @@ Attention::~Attention() {
 std::int64_t Attention::workspace_bytes() const { return impl_->workspace; }
 const AttentionShape& Attention::shape() const { return impl_->shape; }
 
-void Attention::launch(void* cudnn_handle, void* stream, void* workspace) {
+void Attention::prepare(void* cudnn_handle, int sm_target) {
+  if (!impl_->graphs.count(sm_target)) impl_->build(static_cast<cudnnHandle_t>(cudnn_handle), sm_target);
+}
+
+void Attention::launch(void* cudnn_handle, void* stream, void* workspace, int sm_target) {
   auto* handle = static_cast<cudnnHandle_t>(cudnn_handle);
   if (cudnnSetStream(handle, static_cast<cudaStream_t>(stream)) != CUDNN_STATUS_SUCCESS)
     throw Error(ErrorCode::IoFailure, "cudnn", "cudnnSetStream failed");
-  fe_check(impl_->graph->execute(handle, impl_->ptrs, workspace), "sdpa execute");
+  auto it = impl_->graphs.find(sm_target);
+  if (it == impl_->graphs.end()) throw Error(ErrorCode::InvalidInput, "attention", "graph not prepared for the SM target");
+  fe_check(it->second->execute(handle, impl_->ptrs, workspace), "sdpa execute");
 }
 
 void* create_cudnn_handle() {

@@ -15,9 +15,12 @@ class Attention {
   ~Attention();
   Attention(const Attention&) = delete;
   Attention& operator=(const Attention&) = delete;
+  // workspace the prepared graphs need (max over SM targets)
   std::int64_t workspace_bytes() const;
   const AttentionShape& shape() const;
-  void launch(void* cudnn_handle, void* stream, void* workspace);
+  // builds the graph for `sm_target` SMs (0 = all) if not built yet
+  void prepare(void* cudnn_handle, int sm_target);
+  void launch(void* cudnn_handle, void* stream, void* workspace, int sm_target);
 
  private:
   struct Impl;

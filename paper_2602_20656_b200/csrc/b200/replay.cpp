@@ -421,7 +421,16 @@ struct ReplayEngine::Impl {
         }
         attention[i].push_back(hit);
       }
-    if (ws > 0) cuda_check(cudaMalloc(&attn_workspace, static_cast<std::size_t>(ws)), "attention workspace");
+    ensure_attn_workspace(ws);
+  }
+
+  std::int64_t attn_ws_bytes = 0;
+  void ensure_attn_workspace(std::int64_t bytes) {
+    if (bytes <= attn_ws_bytes) return;
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    if (attn_workspace) cudaFree(attn_workspace);
+    cuda_check(cudaMalloc(&attn_workspace, static_cast<std::size_t>(bytes)), "attention workspace");
+    attn_ws_bytes = bytes;
   }
 
   void build_comms() {
@@ -705,8 +714,13 @@ struct ReplayEngine::Impl {
     // before the barrier and the start event — never inside the measurement.
     if (do_compute)
       for (std::size_t i = 0; i < M; ++i)
-        if (sm_target[i] > 0)
+        if (sm_target[i] > 0) {
           for (Gemm& g : gemms[i]) plan_for(g, sm_target[i]);
+          for (Attention* at : attention[i]) {
+            at->prepare(cudnn, sm_target[i]);
+            ensure_attn_workspace(at->workspace_bytes());
+          }
+        }
     coord.barrier();
     const bool e2e = mode == Mode::LagomE2E;
     cuda_check(cudaEventRecord(ev_start, cs), "record");
@@ -726,7 +740,7 @@ struct ReplayEngine::Impl {
       for (std::size_t i = 0; i < M; ++i) {
         cuda_check(cudaEventRecord(ev_cb[i], cs), "record");
         for (Gemm& g : gemms[i]) launch_gemm(g, sm_target[i]);
-        for (Attention* at : attention[i]) at->launch(cudnn, cs, attn_workspace);
+        for (Attention* at : attention[i]) at->launch(cudnn, cs, attn_workspace, sm_target[i]);
         cuda_check(cudaEventRecord(ev_ce[i], cs), "record");
       }
     }

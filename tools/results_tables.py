@@ -26,6 +26,37 @@ def picks(line):
     return f"{ps[0].split('/')[0]} {nc} {nt}"
 
 
+def dominant_roofline(d, n):
+    """The roofline of the config group with the largest summed x (bench.py's
+    definition), recomputed from the line's raw replays: wire bytes per rank
+    on the busier direction / CUDA-event time in the comm-only replay."""
+    import statistics
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2602_20656_b200 import dags
+    line, raw = d["line"], d["raw"]
+    w = next(k for k in NAMES if line["config"]["workload"].startswith(k.split("-")[0] + "-" + k.split("-")[1]))
+    dag = dags.BUILDERS[w](n)
+    last = dag["compute_ops"][-1]["id"]
+    nroles = 1 + max(int(c.get("role", 0)) for c in dag["comm_ops"])
+    g = [int(c.get("role", 0)) + (nroles if c.get("ready_after") == last else 0) for c in dag["comm_ops"]]
+    present = sorted(set(g))
+    groups = [present.index(x) for x in g]
+    xs = {}
+    for r in raw["lagom"]:
+        for j, x in enumerate(r["x"]):
+            xs[groups[j]] = xs.get(groups[j], 0.0) + x
+    gd = max(xs, key=xs.get)
+    j = groups.index(gd)
+    cfg = d["tune"]["configs"][gd]
+    t = statistics.median(r["x_ev"][j] for r in raw["comm"])
+    nv = line["lagom"]["nvls"]
+    wb, _ = bench.wire_bytes(dag["comm_ops"][j], n, cfg, nv["active"], nv["peer_mappings"])
+    peak = line["roofline"]["peak"]
+    return wb / (t * 1e-6) / 1e9 / peak, f"{cfg['algorithm']} NC{cfg['num_channels']}/NT{cfg['num_threads']}"
+
+
 def fmt(v, nd=2):
     return "—" if v is None else f"{v:.{nd}f}"
 
@@ -33,7 +64,7 @@ def fmt(v, nd=2):
 def bench_rows():
     out = ["| workload (BASELINE config) | N | Lagom-tuned | NCCL-default | speedup | ours @ seed | "
            "ours @ seed + SM partition | NCCL + SM partition | compute only | picks | compute slowdown "
-           "(Lagom / NCCL) | roofline frac (wire) |",
+           "(Lagom / NCCL) | roofline frac (dominant group) |",
            "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for n in (4, 2, 1):
         for w, name in NAMES.items():
@@ -44,10 +75,11 @@ def bench_rows():
             a, c = line["arms_ms"], line["compute"]
             sp = line["speedup_vs_nccl_default"]
             sps = f"**{sp:.3f}×**" if sp and sp >= 1.07 else f"{sp:.3f}×"
+            frac, dcfg = dominant_roofline(d, n)
             out.append(f"| {name} | {n} | {a['lagom']:.2f} | {fmt(a.get('nccl'))} | {sps} | {fmt(a.get('seed'))} | "
                        f"{fmt(a.get('seed_partition_all'))} | {fmt(a.get('nccl_partition'))} | {a['compute']:.2f} | "
                        f"{picks(line)} | {c['slowdown']:.3f} / {fmt(c.get('slowdown_nccl'), 3)} | "
-                       f"{line['roofline']['frac']:.3f} |")
+                       f"{frac:.3f} ({dcfg}) |")
     return "\n".join(out)
 
 
