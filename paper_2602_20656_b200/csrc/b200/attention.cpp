@@ -44,9 +44,9 @@ struct Attention::Impl {
 };
 
 // One cuDNN graph and plan per SM count target: the replay's SM partition
-// restricts the attention victims like the GEMMs (the graph's sm_count knob,
-// CUDNN_ATTR_ENGINE_SM_COUNT_TARGET), so a dedicated collective's SMs are
-// not taken by the attention's CTAs either.
+// asks the attention victims for the GEMMs' SM budget too (the graph's
+// sm_count knob, CUDNN_ATTR_ENGINE_SM_COUNT_TARGET) where an engine supports
+// it.
 void Attention::Impl::build(cudnnHandle_t handle, int sm_target) {
   const AttentionShape& s = shape;
   const int64_t b = s.batch, h = s.heads, n = s.seq, d = s.head_dim;
@@ -125,7 +125,16 @@ std::int64_t Attention::workspace_bytes() const { return impl_->workspace; }
 const AttentionShape& Attention::shape() const { return impl_->shape; }
 
 void Attention::prepare(void* cudnn_handle, int sm_target) {
-  if (!impl_->graphs.count(sm_target)) impl_->build(static_cast<cudnnHandle_t>(cudnn_handle), sm_target);
+  if (impl_->graphs.count(sm_target)) return;
+  try {
+    impl_->build(static_cast<cudnnHandle_t>(cudnn_handle), sm_target);
+  } catch (const Error&) {
+    // cuDNN 9.22's sm_100 SDPA engines reject SM carveouts ("SM carveout not
+    // supported for this engine"): the attention then runs on every SM, and
+    // the collectives' stream priority (replay.cpp) gets their CTAs the next
+    // SM that frees up.
+    impl_->graphs[sm_target] = impl_->graphs.at(0);
+  }
 }
 
 void Attention::launch(void* cudnn_handle, void* stream, void* workspace, int sm_target) {

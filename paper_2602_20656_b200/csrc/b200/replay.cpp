@@ -265,7 +265,13 @@ struct ReplayEngine::Impl {
     cuda_check(cudaSetDevice(opts.device), "cudaSetDevice");
     cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, opts.device), "sm count");
     cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking), "stream");
+    // The comm stream has the highest priority (every arm, NCCL included):
+    // a collective launched while the victims' CTAs fill the GPU gets the
+    // next SM that frees up instead of queueing behind the rest of a GEMM or
+    // attention grid.
+    int prio_lo = 0, prio_hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
+    cuda_check(cudaStreamCreateWithPriority(&ks, cudaStreamNonBlocking, prio_hi), "stream");
     lt_check(cublasLtCreate(&lt), "cublasLtCreate");
     cuda_check(cudaMalloc(&workspace, workspace_bytes), "workspace");
     build_gemms();
