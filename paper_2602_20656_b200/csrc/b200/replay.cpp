@@ -567,8 +567,12 @@ struct ReplayEngine::Impl {
     lt_check(cublasLtMatmulAlgoGetHeuristic(lt, desc, g.a, g.b, g.d, g.d, pref, kCands, res, &found), "heuristic");
     cublasLtMatmulPreferenceDestroy(pref);
     if (found < 1) throw Error(ErrorCode::IoFailure, "cublasLt", "no algorithm for the GEMM shape");
-    int best = 0;
-    if (found > 1 && opts.autotune_gemms) {
+    // Rank 0 times the candidates and every rank takes its pick (identical
+    // candidate lists: same device, same cuBLASLt): ranks that ran different
+    // GEMM kernels would drift apart within a layer, and the gated
+    // collectives would then wait for the slowest rank at every step.
+    std::int32_t best = 0;
+    if (found > 1 && opts.autotune_gemms && rank == 0) {
       cudaEvent_t e0, e1;
       cuda_check(cudaEventCreate(&e0), "event");
       cuda_check(cudaEventCreate(&e1), "event");
@@ -595,6 +599,8 @@ struct ReplayEngine::Impl {
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
     }
+    if (opts.autotune_gemms && n > 1) coord.broadcast(&best, sizeof best, 0);
+    if (best >= found) best = 0;
     return algo_cache.emplace(key, res[best].algo).first->second;
   }
 
