@@ -47,11 +47,11 @@ def main():
     xs = [torch.randn(nin, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
     ys = [torch.empty(nout, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
     if n == 1:
-        comm = C.Communicator(0, 1, torch.cuda.current_device())
+        comm = C.Communicator(0, 1, torch.cuda.current_device(), max_channels=64)
         launch = lambda: comm.launch(coll, cfg, C.BF16, a.count, xs[0].data_ptr(), ys[0].data_ptr(),  # noqa: E731
                                      stream.cuda_stream)
     else:
-        comm = C.VirtualCommunicator(n, torch.cuda.current_device())
+        comm = C.VirtualCommunicator(n, torch.cuda.current_device(), max_channels=64)
         launch = lambda: comm.launch(coll, cfg, C.BF16, a.count, [x.data_ptr() for x in xs],  # noqa: E731
                                      [y.data_ptr() for y in ys], stream.cuda_stream)
     for _ in range(3):

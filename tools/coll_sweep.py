@@ -26,7 +26,10 @@ def parse_size(s):
     return int(float(s[:-1] if s[-1] in "KMG" else s) * mul)
 
 
-def time_it(fn, reps, warm, stream):
+def time_it(fn, reps, warm, stream, batch=1):
+    """Median over reps of one timed group of `batch` back-to-back launches,
+    per launch (batch > 1 hides the launch latency and the barrier's rank
+    skew, leaving the kernels' own back-to-back rate)."""
     for _ in range(warm):
         fn()
     times = []
@@ -36,10 +39,11 @@ def time_it(fn, reps, warm, stream):
         dist.barrier()
         torch.cuda.synchronize()
         a.record(stream)
-        fn()
+        for _ in range(batch):
+            fn()
         b.record(stream)
         b.synchronize()
-        times.append(a.elapsed_time(b) / 1e3)
+        times.append(a.elapsed_time(b) / 1e3 / batch)
     times.sort()
     t = torch.tensor([times[len(times) // 2]], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -54,6 +58,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warm", type=int, default=2)
     ap.add_argument("--nccl", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=1, help="launches per timed group (per-launch time reported)")
+    ap.add_argument("--lagom", type=int, default=1, help="0: NCCL rows only (e.g. under NCCL_ALGO=NVLS)")
     ap.add_argument("--out", default="")
     ap.add_argument("--nvls", type=int, default=0, help="buffers in an NVLS region (TREE runs in-switch)")
     ap.add_argument("--use-tma", type=int, default=1, help="SIMPLE data path: 0 LSU, 1 TMA copies, 2 TMA also reduces")
@@ -106,20 +112,20 @@ def main():
                     mag = torch.empty(n_out, device="cuda")
                     dist.reduce_scatter_tensor(y_ref, xf)
                     dist.reduce_scatter_tensor(mag, xa)
-            for spec in args.configs.split(","):
+            for spec in (args.configs.split(",") if args.lagom else []):
                 f = spec.split(":")
                 nc, nt, ch, proto = f[:4]
                 algo = int(f[4]) if len(f) > 4 else C.RING
                 cfg = C.CollConfig(algo, int(proto), int(nc), int(nt), parse_size(ch))
                 fn = lambda: comm.launch(coll, cfg, C.BF16, count, x.data_ptr(), y.data_ptr(), s_ptr)
-                t = time_it(fn, args.reps, args.warm, stream)
+                t = time_it(fn, args.reps, args.warm, stream, args.batch)
                 comm.check()
                 if mag is None:
                     ok = bool(torch.equal(y, y_ref))
                 else:
                     ok = bool(((y.float() - y_ref).abs() <= (2.0 ** -7) * world * mag + 1e-6).all())
                 rows.append(dict(impl="lagom", ok=ok, coll=cn, algo=int(algo), proto=int(proto), nc=int(nc), nt=int(nt),
-                                 use_tma=args.use_tma,
+                                 use_tma=args.use_tma, nvls=args.nvls, batch=args.batch,
                                  chunk=parse_size(ch), bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
                                  busbw=s_bytes / t * fac / 1e9))
                 if rank == 0:
@@ -133,8 +139,9 @@ def main():
                     fn = lambda: dist.reduce_scatter_tensor(y, x)
                 else:
                     fn = lambda: dist.all_to_all_single(y, x)
-                t = time_it(fn, args.reps, args.warm, stream)
-                rows.append(dict(impl="nccl", coll=cn, bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
+                t = time_it(fn, args.reps, args.warm, stream, args.batch)
+                rows.append(dict(impl="nccl", algo_env=os.environ.get("NCCL_ALGO", ""), batch=args.batch, coll=cn,
+                                 bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
                                  busbw=s_bytes / t * fac / 1e9))
                 if rank == 0:
                     print(json.dumps(rows[-1]), flush=True)

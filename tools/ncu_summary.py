@@ -42,10 +42,12 @@ def launches(path):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki]
-        if "coll_kernel" in name:
-            key = "lagom coll_kernel (sm_100a collectives)"
-        elif "fill_kernel" in name:
-            key = "lagom fill_kernel (synthetic data, setup only)"
+        if any(k in name for k in ("coll_kernel", "local_copy_kernel", "nvls_kernel", "a2a_tma_kernel")):
+            key = "lagom collectives (sm_100a)"
+        elif "fill_kernel" in name or "timestamp_kernel" in name:
+            key = "lagom fill / timestamp kernels (setup only)"
+        elif "cudnn" in name or "sdpa" in name:
+            key = "cuDNN SDPA attention (victims)"
         else:
             key = "cuBLASLt GEMMs (victims)"
         tot[key] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
@@ -59,8 +61,9 @@ def main():
     ap.add_argument("--label", action="append", default=[])
     ap.add_argument("--launches", default="")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--title", default="round 2")
     a = ap.parse_args()
-    md = ["# ncu summaries (round 1)", ""]
+    md = [f"# ncu summaries ({a.title})", ""]
     for i, rep in enumerate(a.rep):
         label = a.label[i] if i < len(a.label) else rep
         md += [f"## {label}", "", f"source: `{rep}` (`ncu --set full --clock-control none`)", ""]
