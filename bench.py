@@ -262,7 +262,12 @@ def wire_bytes(op: dict, n: int, cfg: dict, nvls: bool, one_hop_a2a: bool, one_h
     tree = cfg["algorithm"] == "TREE"
     if tree and nvls and one_hop_agrs and coll in ("ALL_GATHER", "REDUCE_SCATTER"):
         return S * (n - 1) / n, "one hop (peer stores / pushes): (n-1)/n S egress"
-    if tree and nvls and coll in ("ALL_REDUCE", "ALL_GATHER", "REDUCE_SCATTER"):
+    if tree and nvls and coll == "ALL_REDUCE":
+        # ld_reduce: every GPU serves each rank's S/n share (S out); multimem.st:
+        # the switch delivers every share to every GPU (S in), plus the own share
+        # each way: S (1 + 1/n) per rank on either direction
+        return S * (n + 1) / n, "NVLS AllReduce (in-switch): S (1 + 1/n) per rank per direction"
+    if tree and nvls and coll in ("ALL_GATHER", "REDUCE_SCATTER"):
         return float(S), "NVLS (in-switch): S per rank on the busier direction"
     if tree and coll == "ALL_TO_ALL" and one_hop_a2a:
         return S * (n - 1) / n, "one-hop AllToAll: (n-1)/n S egress"

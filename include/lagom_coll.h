@@ -213,6 +213,15 @@ int lagom_fill_random(void* ptr, int64_t nelems, int dtype, uint64_t seed, float
  * device uint64 at `dst`: aligns stream timelines with counter samples. */
 int lagom_timestamp(void* dst, void* stream);
 
+/* Diagnostics. With LAGOM_PHASE_STAMPS=1 in the environment at communicator
+ * creation, the switch kernels (NVLS AR / AG / RS, one hop) record per channel
+ * for the last two launches 8 uint64 values: %globaltimer at entry, after the entry
+ * barrier, after the data loop, after the system fence, after the exit
+ * barrier, then the launch's epoch. Synchronizes the device and copies
+ * min(max_values, max_channels * 16) of them, [channel][(epoch/2)%2][8], into
+ * `out`. */
+int lagom_comm_phase_stamps(lagom_comm_t comm, uint64_t* out, int max_values);
+
 #ifdef __cplusplus
 }
 #endif

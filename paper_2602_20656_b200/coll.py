@@ -73,7 +73,7 @@ EXPORTED_SYMBOLS = (
     "lagom_comm_nvls_supported", "lagom_comm_nvls_export", "lagom_comm_nvls_import",
     "lagom_comm_nvls_bind", "lagom_comm_nvls_alloc", "lagom_comm_nvls_bytes",
     "lagom_comm_nvls_export_peer", "lagom_comm_nvls_import_peers", "lagom_comm_nvls_use_peers",
-    "lagom_coll_footprint", "lagom_timestamp", "lagom_comm_nvls_scratch",
+    "lagom_coll_footprint", "lagom_timestamp", "lagom_comm_nvls_scratch", "lagom_comm_phase_stamps",
 )
 
 _lib = None
@@ -120,6 +120,7 @@ def library() -> ctypes.CDLL:
         "lagom_comm_nvls_use_peers": (c_int, [vp, c_int]),
         "lagom_timestamp": (c_int, [vp, vp]),
         "lagom_comm_nvls_scratch": (c_int, [vp, c_i64]),
+        "lagom_comm_phase_stamps": (c_int, [vp, ctypes.POINTER(ctypes.c_uint64), c_int]),
         "lagom_coll_footprint": (c_int, [vp, ctypes.POINTER(_Args), vp, vp, ctypes.POINTER(c_int),
                                          ctypes.POINTER(c_int)]),
     }
@@ -320,6 +321,16 @@ class Communicator:
 
     def check(self) -> None:
         _check(library().lagom_comm_check(self._h), "comm")
+
+    def phase_stamps(self, max_channels: int) -> list:
+        """Diagnostics (LAGOM_PHASE_STAMPS=1 at creation): per channel, for the
+        last two launches (by epoch parity), the switch kernels' %globaltimer
+        stamps [entry, entry barrier done, data done, fence done, exit barrier
+        done] and the launch epoch. Synchronizes the device."""
+        n = max_channels * 2 * 8
+        buf = (ctypes.c_uint64 * n)()
+        _check(library().lagom_comm_phase_stamps(self._h, buf, n), "phase_stamps")
+        return [[list(buf[(c * 2 + k) * 8:(c * 2 + k) * 8 + 8]) for k in range(2)] for c in range(max_channels)]
 
     def close(self) -> None:
         if self._h:

@@ -75,6 +75,8 @@ void layout(lagom_comm* c) {
   off += ch * n * 128;
   c->off_nvpbase = off;  // push RS: pieces completed per channel so far (local)
   off += ch * 8;
+  c->off_phase = off;  // diagnostics: per-channel phase stamps, 2 launches (local)
+  off += ch * 2 * LAGOM_PHASE_STAMPS * 8;
   off = (off + 4095) / 4096 * 4096;
   c->off_slots = off;
   off += ch * n * c->opts.steps * c->slot_bytes;
@@ -103,6 +105,8 @@ int alloc_common(lagom_comm* c) {
   cudaEvent_t ev;
   LAGOM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   c->order_ev = ev;
+  const char* ps = std::getenv("LAGOM_PHASE_STAMPS");
+  c->phase_stamps = ps && std::atoi(ps) > 0 ? 1 : 0;
   return LAGOM_OK;
 }
 
@@ -524,3 +528,13 @@ int lagom_coll_bytes(const lagom_coll_args_t* a, int nranks, int64_t* alg_bytes,
 }
 
 }  // extern "C"
+
+extern "C" int lagom_comm_phase_stamps(lagom_comm_t comm, uint64_t* out, int max_values) {
+  if (!comm || !out || max_values < 0) return fail(LAGOM_ERR_INVALID_ARGUMENT, "phase_stamps: bad argument");
+  const int64_t total = static_cast<int64_t>(comm->opts.max_channels) * 2 * LAGOM_PHASE_STAMPS;
+  const int64_t n = std::min<int64_t>(total, max_values);
+  LAGOM_CUDA(cudaSetDevice(comm->device));
+  LAGOM_CUDA(cudaDeviceSynchronize());
+  LAGOM_CUDA(cudaMemcpy(out, comm->heap[comm->virt ? 0 : comm->rank] + comm->off_phase, n * 8, cudaMemcpyDeviceToHost));
+  return LAGOM_OK;
+}

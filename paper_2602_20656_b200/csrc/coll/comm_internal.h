@@ -5,6 +5,11 @@
 
 #include "lagom_coll.h"
 
+// Stamps per channel and launch recorded by the switch kernels when
+// LAGOM_PHASE_STAMPS=1 (lagom_comm_phase_stamps): entry, entry barrier done,
+// data done, fence done, exit barrier done, epoch.
+constexpr int LAGOM_PHASE_STAMPS = 8;
+
 struct lagom_comm {
   int rank = 0;
   int nranks = 1;
@@ -36,6 +41,8 @@ struct lagom_comm {
   bool nvls_ready = false;
   int64_t off_nvbar = 0, off_nvep = 0;      // NVLS barrier flags / epochs in the heap
   int64_t off_nvpiece = 0, off_nvpbase = 0; // push RS piece flags / per-channel piece counts
+  int64_t off_phase = 0;                    // phase stamps of the switch kernels (diagnostics)
+  int phase_stamps = 0;                     // LAGOM_PHASE_STAMPS=1 at creation: kernels record them
   int nvls_export_fd = -1;                  // rank 0's exported fd, closed once bound
   // Peer (unicast) mappings of every rank's region: one-hop AllToAll writes
   // straight into the destination rank's recv buffer.

@@ -77,7 +77,6 @@ size_t granularity(int nranks) {
 // --------------------------------------------------------------- kernels ---
 using lagom_dev::globaltimer;
 using lagom_dev::ld_acquire_sys;
-using lagom_dev::st_release_sys;
 
 struct NvlsParams {
   char* heap[LAGOM_MAX_RANKS];
@@ -99,13 +98,22 @@ struct NvlsParams {
   const char* peer_send[LAGOM_MAX_RANKS];  // one-hop RS (pull): send in every rank's region
   char* scratch;                           // push RS: my scratch (slot q holds rank q's partial)
   int64_t scratch_slot;                    // bytes per scratch slot
+  uint64_t* phase;                         // diagnostics: [ch][parity][LAGOM_PHASE_STAMPS] or null
 };
 
+// Thread 0 records stamp k of this channel's launch (lagom_comm_phase_stamps);
+// epochs advance by 2 per launch, so (ep >> 1) & 1 alternates.
+__device__ __forceinline__ void phase_stamp(const NvlsParams& P, int ch, uint64_t ep, int k) {
+  if (P.phase) P.phase[(static_cast<int64_t>(ch) * 2 + ((ep >> 1) & 1)) * LAGOM_PHASE_STAMPS + k] = globaltimer();
+}
+
+// Polls *p (relaxed) until it reaches v; the caller then reads it once with
+// ld.acquire (acquire pattern). false on abort or timeout.
 __device__ bool nv_wait(const uint64_t* p, uint64_t v, const NvlsParams& P) {
   uint64_t t0 = 0;
   unsigned it = 0;
-  while (ld_acquire_sys(p) < v) {
-    if ((++it & 127u) == 0) {
+  while (lagom_dev::ld_relaxed_sys(p) < v) {
+    if ((++it & 255u) == 0) {
       if (*reinterpret_cast<volatile unsigned*>(P.abort_flag)) return false;
       const uint64_t now = globaltimer();
       if (!t0) t0 = now;
@@ -118,18 +126,33 @@ __device__ bool nv_wait(const uint64_t* p, uint64_t v, const NvlsParams& P) {
   return true;
 }
 
-// All ranks' CTA `ch` meet: each posts `ep` into every peer's flag [ch][me]
-// and waits for every peer's post. Runs on thread 0.
-__device__ bool nv_barrier(const NvlsParams& P, int ch, uint64_t ep) {
-  const int n = P.nranks, r = P.rank;
-  for (int p = 0; p < n; ++p)
-    if (p != r)
-      st_release_sys(reinterpret_cast<uint64_t*>(P.heap[p] + P.off_nvbar + (static_cast<int64_t>(ch) * n + r) * 128), ep);
-  for (int p = 0; p < n; ++p)
-    if (p != r &&
-        !nv_wait(reinterpret_cast<const uint64_t*>(P.heap[r] + P.off_nvbar + (static_cast<int64_t>(ch) * n + p) * 128), ep, P))
-      return false;
-  return true;
+// All ranks' CTA `ch` meet. Every thread of the CTA calls it. Threads
+// 0..n-2 work in parallel: thread t posts `ep` into peer p = r+1+t's flag
+// [ch][me] (relaxed) and polls its own flag [ch][p] (relaxed), then reads it
+// once more with ld.acquire (the peer's writes before its post). With
+// `release` (exit barriers), thread 0 first runs ONE system fence for the
+// CTA after a __syncthreads, which releases every thread's earlier writes
+// (multimem / peer stores) before any post. System fences are the expensive
+// part and contend across SMs (tools/flag_latency.cu on 4xB200, per barrier:
+// a fence per post as in st.release 5.5 us at 64 CTAs, relaxed posts 1.6 us,
+// one fence per CTA 4.4-5.6 us at 8-64 CTAs; profiles/round2_nvls_phases.md).
+__device__ bool nv_barrier(const NvlsParams& P, int ch, uint64_t ep, int* s_ok, bool release) {
+  const int n = P.nranks, r = P.rank, t = threadIdx.x;
+  __syncthreads();
+  if (t == 0) {
+    *s_ok = 1;
+    if (release) lagom_dev::fence_acq_rel_sys();
+  }
+  __syncthreads();
+  if (t < n - 1) {
+    const int p = (r + 1 + t) % n;
+    const uint64_t* mine = reinterpret_cast<const uint64_t*>(P.heap[r] + P.off_nvbar + (static_cast<int64_t>(ch) * n + p) * 128);
+    lagom_dev::st_relaxed_sys(reinterpret_cast<uint64_t*>(P.heap[p] + P.off_nvbar + (static_cast<int64_t>(ch) * n + r) * 128), ep);
+    if (!nv_wait(mine, ep, P)) *s_ok = 0;
+    else (void)ld_acquire_sys(mine);
+  }
+  __syncthreads();
+  return *s_ok != 0;
 }
 
 template <typename T> struct Mm;
@@ -185,9 +208,9 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
   if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
   uint64_t* ep_home = reinterpret_cast<uint64_t*>(P.heap[r] + P.off_nvep + static_cast<int64_t>(ch) * 8);
   const uint64_t ep = *reinterpret_cast<volatile uint64_t*>(ep_home) + 1;
-  if (threadIdx.x == 0) s_ok = nv_barrier(P, ch, ep) ? 1 : 0;  // every rank's inputs are ready
-  __syncthreads();
-  if (!s_ok) return;
+  if (threadIdx.x == 0) phase_stamp(P, ch, ep, 0);
+  if (!nv_barrier(P, ch, ep, &s_ok, false)) return;  // every rank's inputs are ready
+  if (threadIdx.x == 0) phase_stamp(P, ch, ep, 1);
 
   // 16 B units: AR/RS reduce the whole buffer / own block through the switch,
   // AG broadcasts the own block, A2A (KIND 3) writes block p straight into
@@ -298,26 +321,23 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
         for (; left > 0; left -= nt, src += nt, dst += nt) *dst = *src;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence_system();  // the piece's peer stores before its flag
-        for (int k = 1; k < n; ++k) {
-          const int p = (r + k) % n;
-          st_release_sys(reinterpret_cast<uint64_t*>(P.heap[p] + P.off_nvpiece + (static_cast<int64_t>(ch) * n + r) * 128),
-                         pbase + static_cast<uint64_t>(i) + 1);
-        }
+      if (threadIdx.x == 0) lagom_dev::fence_acq_rel_sys();  // the piece's peer stores (every thread's) before its flag
+      __syncthreads();
+      if (threadIdx.x < n - 1) {  // post piece i to every peer, one thread per peer
+        const int p = (r + 1 + threadIdx.x) % n;
+        lagom_dev::st_relaxed_sys(reinterpret_cast<uint64_t*>(P.heap[p] + P.off_nvpiece + (static_cast<int64_t>(ch) * n + r) * 128),
+                                  pbase + static_cast<uint64_t>(i) + 1);
       }
     };
+    if (threadIdx.x == 0) s_go = 1;  // published by push(0)'s __syncthreads
     if (npieces > 0) push(0);
     for (int64_t i = 0; i < npieces; ++i) {
       if (i + 1 < npieces) push(i + 1);
-      if (threadIdx.x == 0) {  // every peer's piece i landed in my scratch
-        bool ok = true;
-        for (int k = 1; k < n && ok; ++k) {
-          const int q = (r + k) % n;
-          ok = nv_wait(reinterpret_cast<const uint64_t*>(P.heap[r] + P.off_nvpiece + (static_cast<int64_t>(ch) * n + q) * 128),
-                       pbase + static_cast<uint64_t>(i) + 1, P);
-        }
-        s_go = ok ? 1 : 0;
+      if (threadIdx.x < n - 1) {  // every peer's piece i landed in my scratch
+        const int q = (r + 1 + threadIdx.x) % n;
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(P.heap[r] + P.off_nvpiece + (static_cast<int64_t>(ch) * n + q) * 128);
+        if (!nv_wait(f, pbase + static_cast<uint64_t>(i) + 1, P)) s_go = 0;
+        else (void)ld_acquire_sys(f);
       }
       __syncthreads();
       if (!s_go) return;
@@ -437,12 +457,18 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
       if (u0 + k * nt < hi) store(out + (u0 + k * nt) * 16, v[k]);
   }
   }
-  __syncthreads();
+  if (P.phase) {
+    __syncthreads();
+    if (threadIdx.x == 0) phase_stamp(P, ch, ep, 2);
+  }
+  // my multimem / peer stores are visible everywhere before any rank moves
+  // on: nobody reads results or reuses inputs early
+  const bool done = nv_barrier(P, ch, ep + 1, &s_ok, true);
   if (threadIdx.x == 0) {
-    __threadfence_system();  // my multimem / peer stores are visible everywhere
-    // nobody reads results or reuses inputs early
-    s_ok = nv_barrier(P, ch, ep + 1) ? 1 : 0;
-    if (s_ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    if (done) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    phase_stamp(P, ch, ep, 3);
+    phase_stamp(P, ch, ep, 4);
+    if (P.phase) P.phase[(static_cast<int64_t>(ch) * 2 + ((ep >> 1) & 1)) * LAGOM_PHASE_STAMPS + 5] = ep;
   }
   if (threadIdx.x == 0 && P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
 }
@@ -468,10 +494,8 @@ __global__ void __launch_bounds__(640) a2a_tma_kernel(const __grid_constant__ Nv
   if (threadIdx.x == 0) {
     for (int s = 0; s < kA2aStages; ++s) lagom_dev::mbar_init(&full[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_ok = nv_barrier(P, ch, ep) ? 1 : 0;  // every rank's recv is free
   }
-  __syncthreads();
-  if (!s_ok) return;
+  if (!nv_barrier(P, ch, ep, &s_ok, false)) return;  // every rank's recv is free
   if (threadIdx.x == 0) {
     const int64_t blk = P.count * P.elem_bytes;  // bytes per block (16 B multiple)
     const int64_t units = blk / 16, per_ch = (units + nch - 1) / nch;
@@ -512,11 +536,9 @@ __global__ void __launch_bounds__(640) a2a_tma_kernel(const __grid_constant__ Nv
     lagom_dev::bulk_wait_all();        // every bulk store performed
     lagom_dev::fence_proxy_global();   // async-proxy writes -> generic proxy
   }
-  __syncthreads();
+  const bool done = nv_barrier(P, ch, ep + 1, &s_ok, true);  // every peer's writes into my recv landed
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    const bool ok = nv_barrier(P, ch, ep + 1);  // every peer's writes into my recv landed
-    if (ok) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    if (done) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
     if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
   }
 }
@@ -678,6 +700,7 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   p.abort_flag = c->abort_dev;
   p.timeout_ns = static_cast<uint64_t>(c->opts.timeout_ms) * 1000000ull;
   p.span = static_cast<unsigned long long*>(a->span_out);
+  p.phase = c->phase_stamps ? reinterpret_cast<uint64_t*>(c->heap[c->rank] + c->off_phase) : nullptr;
   std::memcpy(params_out, &p, sizeof p);
   *params_bytes = sizeof p;
   *kernel = k;
