@@ -73,7 +73,7 @@ def test_counter_model_rows_reproduce(tmp_path, n):
     committed_path = os.path.join(ROOT, "profiles", f"round2_model_n{n}.json")
     subprocess.run([sys.executable, os.path.join(ROOT, "tools", "counter_fit.py"), "--n", str(n),
                     "--profiles", os.path.join(ROOT, "profiles", f"round2_counters_n{n}_*.json"),
-                    "--bench", os.path.join(ROOT, "profiles", f"round2_final_n{n}_*.json"),
+                    "--bench", os.path.join(ROOT, "profiles", f"round2_session3_n{n}_*.json"),
                     "--globals", committed_path, "--out", str(out)], cwd=ROOT, check=True, capture_output=True,
                    timeout=900)
     got, committed = json.load(open(out)), json.load(open(committed_path))

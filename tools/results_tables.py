@@ -1,6 +1,8 @@
 """Prints DESIGN.md §6's result tables from the committed round-2 files:
-bench lines (profiles/round2_final_n{N}_{workload}.json) and the
-counter-backed model (profiles/round2_model_n{N}.json). No GPU.
+bench lines (profiles/round2_final_n{N}_{workload}.json, and the same
+session's repeat round2_final_rep2_n{N}_{workload}.json) and the
+counter-backed model (profiles/round2_model_n{N}.json, fitted to the
+counter profiles and the bench lines of session 3, round2_session3_*). No GPU.
 
   python tools/results_tables.py
 """
@@ -64,8 +66,8 @@ def fmt(v, nd=2):
 def bench_rows():
     out = ["| workload (BASELINE config) | N | Lagom-tuned | NCCL-default | speedup | ours @ seed | "
            "ours @ seed + SM partition | NCCL + SM partition | compute only | picks | compute slowdown "
-           "(Lagom / NCCL) | roofline frac (dominant group) |",
-           "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+           "(Lagom / NCCL) | roofline frac (dominant group) | repeat: speedup, picks |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for n in (4, 2, 1):
         for w, name in NAMES.items():
             d = load(f"round2_final_n{n}_{w}.json")
@@ -76,10 +78,15 @@ def bench_rows():
             sp = line["speedup_vs_nccl_default"]
             sps = f"**{sp:.3f}×**" if sp and sp >= 1.07 else f"{sp:.3f}×"
             frac, dcfg = dominant_roofline(d, n)
+            d2 = load(f"round2_final_rep2_n{n}_{w}.json")
+            rep = "—"
+            if d2:
+                sp2 = d2["line"]["speedup_vs_nccl_default"]
+                rep = (f"**{sp2:.3f}×**" if sp2 >= 1.07 else f"{sp2:.3f}×") + f", {picks(d2['line'])}"
             out.append(f"| {name} | {n} | {a['lagom']:.2f} | {fmt(a.get('nccl'))} | {sps} | {fmt(a.get('seed'))} | "
                        f"{fmt(a.get('seed_partition_all'))} | {fmt(a.get('nccl_partition'))} | {a['compute']:.2f} | "
                        f"{picks(line)} | {c['slowdown']:.3f} / {fmt(c.get('slowdown_nccl'), 3)} | "
-                       f"{frac:.3f} ({dcfg}) |")
+                       f"{frac:.3f} ({dcfg}) | {rep} |")
     return "\n".join(out)
 
 
