@@ -298,9 +298,11 @@ def main():
                          "collectives whose CTAs cannot share an SM with a GEMM CTA (default), 2 always")
     ap.add_argument("--coresident", type=int, default=1,
                     help="NVLS / one-hop / single-rank kernels sized to co-reside with GEMM CTAs")
-    ap.add_argument("--one-hop", type=int, default=0,
-                    help="lagom_comm_opts_t.one_hop: TREE AG/RS through the switch (0), one hop (1), one hop at n = 2 (2)")
-    ap.add_argument("--a2a-tma", type=int, default=1, help="lagom_comm_opts_t.a2a_tma (one-hop AllToAll via TMA)")
+    ap.add_argument("--one-hop", type=int, default=2,
+                    help="lagom_comm_opts_t.one_hop: TREE AG/RS through the switch (0), one hop (1), one hop at "
+                         "n = 2 (2, default: the switch echoes the own block, so at n = 2 it moves twice the bytes)")
+    ap.add_argument("--a2a-tma", type=int, default=1,
+                    help="lagom_comm_opts_t.a2a_tma (one-hop AllToAll / AllGather / ReduceScatter via TMA)")
     ap.add_argument("--ablations", type=int, default=1,
                     help="also time: our kernels at the seed with the SM partition forced on, and (N > 1) NCCL "
                          "with the GEMMs on num_sms - NCCL's channels")

@@ -147,7 +147,7 @@ struct ReplayOptions {
   // lagom_comm_opts_t.coresident / one_hop / a2a_tma (kernel selection; the
   // same on every rank).
   bool coresident = true;
-  int one_hop = 0;
+  int one_hop = 2;
   bool a2a_tma = true;
   // NVSwitch multicast: comm buffers live in an NVLS region, so TREE
   // AllReduce/AllGather/ReduceScatter run reduced/broadcast in the switch.

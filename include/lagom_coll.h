@@ -72,15 +72,17 @@ typedef struct {
                               shared memory), so their NC costs no SMs; larger NT runs
                               the deep-unroll kernels that take an SM each. 0: deep
                               unrolls at every NT (lagom_coll_footprint tells which) */
-  int one_hop;             /* TREE AllGather / ReduceScatter with NVLS bound: 0 (default)
-                              through the switch, 1 one hop over the peer mappings
-                              (AG: peer stores; RS: pushes into the owners' scratch, see
-                              lagom_comm_nvls_scratch), 2 one hop at nranks == 2 (where
-                              the multicast echo caps the switch schedules)           */
-  int a2a_tma;             /* 1 (default): the one-hop AllToAll moves data with TMA bulk
-                              copies (one elected thread, 192 KB smem ring: the CTA takes
-                              an SM) except in the co-resident regime (coresident and NT
-                              <= 256), which keeps vector stores; 0: vector stores always */
+  int one_hop;             /* TREE AllGather / ReduceScatter with NVLS bound: 0 through
+                              the switch, 1 one hop over the peer mappings
+                              (AG: peer stores; RS: TMA pull of the peers' partials, or
+                              pushes into the owners' scratch with vector stores, see
+                              lagom_comm_nvls_scratch), 2 (default) one hop at nranks == 2
+                              (where the multicast echo doubles the switch's bytes)   */
+  int a2a_tma;             /* 1 (default): the one-hop kernels (AllToAll, and with one_hop
+                              the AllGather / ReduceScatter) move data with TMA bulk copies
+                              (one elected thread, 192 KB smem ring: the CTA takes an SM)
+                              except in the co-resident regime (coresident and NT <= 256),
+                              which keeps vector loads / stores; 0: vector always     */
 } lagom_comm_opts_t;
 
 typedef struct {

@@ -186,7 +186,7 @@ class Communicator:
 
     def __init__(self, rank: int, nranks: int, device: int, *, max_channels: int = 32,
                  steps: int = 4, max_chunk_bytes: int = 4 << 20, timeout_ms: int = 10000,
-                 use_tma: int = 1, coresident: int = 1, one_hop: int = 0, a2a_tma: int = 1):
+                 use_tma: int = 1, coresident: int = 1, one_hop: int = 2, a2a_tma: int = 1):
         lib = library()
         opts = _Opts(max_channels, steps, max_chunk_bytes, timeout_ms, int(use_tma), int(coresident),
                      int(one_hop), int(a2a_tma))

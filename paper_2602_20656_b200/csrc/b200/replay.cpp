@@ -518,7 +518,9 @@ struct ReplayEngine::Impl {
         ok = agree(lagom_comm_nvls_import(lcomm, blob) == LAGOM_OK);
       }
       if (ok) ok = agree(lagom_comm_nvls_bind(lcomm) == LAGOM_OK);
-      if (ok && opts.one_hop && rs_slot > 0) coll_check(lagom_comm_nvls_scratch(lcomm, rs_slot), "nvls scratch");
+      // push ReduceScatter scratch (co-resident one-hop configs) only where one hop applies
+      const bool hop = opts.one_hop == 1 || (opts.one_hop == 2 && n == 2);
+      if (ok && hop && rs_slot > 0) coll_check(lagom_comm_nvls_scratch(lcomm, rs_slot), "nvls scratch");
       nvls_on = ok;
       if (ok) {  // peer mappings: one-hop AllToAll (TREE) into the peers' recv buffers
         unsigned char mine[LAGOM_HANDLE_BYTES];

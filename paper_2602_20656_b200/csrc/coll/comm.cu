@@ -259,7 +259,7 @@ void lagom_comm_default_opts(lagom_comm_opts_t* o) {
   o->timeout_ms = 10000;
   o->use_tma = 1;
   o->coresident = 1;
-  o->one_hop = 0;
+  o->one_hop = 2;
   o->a2a_tma = 1;
 }
 

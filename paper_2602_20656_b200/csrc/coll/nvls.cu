@@ -543,6 +543,152 @@ __global__ void __launch_bounds__(640) a2a_tma_kernel(const __grid_constant__ Nv
   }
 }
 
+// One-hop AllGather through the TMA engine (one_hop with the TMA data path):
+// thread 0 loads each tile of the own block once into a ring of smem stages
+// and bulk-stores it into every rank's recv (the peers' over NVLink, its own
+// last), one bulk group per tile. (n-1)/n S leaves each GPU, against S for
+// the switch's multicast, which also echoes the own block.
+__global__ void __launch_bounds__(640) ag_tma_kernel(const __grid_constant__ NvlsParams P) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ uint64_t full[kA2aStages];
+  __shared__ int s_ok;
+  const int ch = blockIdx.x, nch = gridDim.x, n = P.nranks, r = P.rank;
+  if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
+  uint64_t* ep_home = reinterpret_cast<uint64_t*>(P.heap[r] + P.off_nvep + static_cast<int64_t>(ch) * 8);
+  const uint64_t ep = *reinterpret_cast<volatile uint64_t*>(ep_home) + 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kA2aStages; ++s) lagom_dev::mbar_init(&full[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!nv_barrier(P, ch, ep, &s_ok, false)) return;  // every rank's recv is free
+  if (threadIdx.x == 0) {
+    const int64_t blk = P.count * P.elem_bytes;
+    const int64_t units = blk / 16, per_ch = (units + nch - 1) / nch;
+    const int64_t lo = lagom_dev::lmin(units, per_ch * ch) * 16, hi = lagom_dev::lmin(units, per_ch * (ch + 1)) * 16;
+    const int64_t ntiles = (hi - lo + kA2aTile - 1) / kA2aTile;
+    auto issue = [&](int64_t i) {
+      const int64_t off = lo + i * kA2aTile;
+      const uint32_t len = static_cast<uint32_t>(lagom_dev::lmin(kA2aTile, hi - off));
+      const int st = static_cast<int>(i % kA2aStages);
+      lagom_dev::mbar_expect(&full[st], len);
+      lagom_dev::bulk_load(ring + st * kA2aTile, P.send_uc + off, len, &full[st]);
+    };
+    for (int64_t i = 0; i < ntiles && i < kA2aStages; ++i) issue(i);
+    for (int64_t i = 0; i < ntiles; ++i) {
+      const int st = static_cast<int>(i % kA2aStages);
+      const int64_t off = lo + i * kA2aTile;
+      const uint32_t len = static_cast<uint32_t>(lagom_dev::lmin(kA2aTile, hi - off));
+      lagom_dev::mbar_wait(&full[st], static_cast<uint32_t>((i / kA2aStages) & 1));
+      for (int k = 1; k <= n; ++k) lagom_dev::bulk_store(P.peer_recv[(r + k) % n] + r * blk + off, ring + st * kA2aTile, len);
+      lagom_dev::bulk_commit();
+      if (i >= 1 && i - 1 + kA2aStages < ntiles) {
+        lagom_dev::bulk_wait_read1();  // tile i-1's stores have read its stage
+        issue(i - 1 + kA2aStages);
+      }
+    }
+    lagom_dev::bulk_wait_all();
+    lagom_dev::fence_proxy_global();
+  }
+  const bool done = nv_barrier(P, ch, ep + 1, &s_ok, true);  // every peer's stores into my recv landed
+  if (threadIdx.x == 0) {
+    if (done) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+  }
+}
+
+// One-hop ReduceScatter pulled through the TMA engine: thread 0 bulk-loads,
+// per tile of the own block r, every rank's partial (the peers' over
+// NVLink, from their send buffers in the region) into one smem stage, up to
+// kA2aStages tiles ahead — up to 192 KB of remote reads in flight per SM
+// without registers, where vector loads would be latency-bound. All threads
+// then combine the stage in the ring order (acc = x_{r+1}, then x_{r+2}, ...,
+// ending with the own x_r, rounding to the element type at every combine),
+// so the result is bit-identical to the ring schedule and its oracle, and
+// store it to recv. (n-1)/n S enters each GPU; nothing is pushed.
+template <typename T>
+__global__ void __launch_bounds__(640) rs_tma_kernel(const __grid_constant__ NvlsParams P) {
+  using R = lagom_dev::Red<T, LAGOM_SUM>;
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ uint64_t full[kA2aStages];
+  __shared__ int s_ok;
+  const int ch = blockIdx.x, nch = gridDim.x, n = P.nranks, r = P.rank;
+  if (threadIdx.x == 0 && P.span) atomicMin(P.span, static_cast<unsigned long long>(globaltimer()));
+  uint64_t* ep_home = reinterpret_cast<uint64_t*>(P.heap[r] + P.off_nvep + static_cast<int64_t>(ch) * 8);
+  const uint64_t ep = *reinterpret_cast<volatile uint64_t*>(ep_home) + 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kA2aStages; ++s) lagom_dev::mbar_init(&full[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!nv_barrier(P, ch, ep, &s_ok, false)) return;  // every rank's partials are ready
+  const int64_t blk = P.count * P.elem_bytes;
+  const int64_t units = blk / 16, per_ch = (units + nch - 1) / nch;
+  const int64_t lo = lagom_dev::lmin(units, per_ch * ch) * 16, hi = lagom_dev::lmin(units, per_ch * (ch + 1)) * 16;
+  const int64_t tile = (kA2aTile / n) & ~static_cast<int64_t>(127);  // per partial; n of them per stage
+  const int64_t ntiles = (hi - lo + tile - 1) / tile;
+  auto src = [&](int k) -> const char* {  // partial x_{r+k} of my block
+    const int q = (r + k) % n;
+    return (q == r ? P.send_uc : P.peer_send[q]) + r * blk;
+  };
+  auto issue = [&](int64_t i) {
+    const int64_t off = lo + i * tile;
+    const uint32_t len = static_cast<uint32_t>(lagom_dev::lmin(tile, hi - off));
+    const int st = static_cast<int>(i % kA2aStages);
+    lagom_dev::mbar_expect(&full[st], len * static_cast<uint32_t>(n));
+    for (int k = 1; k <= n; ++k)
+      lagom_dev::bulk_load(ring + st * kA2aTile + (k - 1) * tile, src(k) + off, len, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < ntiles && i < kA2aStages; ++i) issue(i);
+  for (int64_t i = 0; i < ntiles; ++i) {
+    const int st = static_cast<int>(i % kA2aStages);
+    const int64_t off = lo + i * tile;
+    const int64_t len = lagom_dev::lmin(tile, hi - off);
+    lagom_dev::mbar_wait(&full[st], static_cast<uint32_t>((i / kA2aStages) & 1));
+    const uint4* x = reinterpret_cast<const uint4*>(ring + st * kA2aTile);
+    const int64_t tu = tile / 16;
+    uint4* out = reinterpret_cast<uint4*>(P.recv_uc + off);
+    for (int64_t u = threadIdx.x; u < len / 16; u += blockDim.x) {
+      uint4 acc = x[u];
+      for (int k = 2; k <= n; ++k) acc = lagom_dev::red4<R>(x[(k - 1) * tu + u], acc);
+      out[u] = acc;
+    }
+    __syncthreads();  // the stage is consumed
+    if (threadIdx.x == 0 && i + kA2aStages < ntiles) issue(i + kA2aStages);
+  }
+  // my loads of the peers' send buffers completed (their mbarrier fired):
+  // the peers may reuse them once every rank posted; no writes to release
+  const bool done = nv_barrier(P, ch, ep + 1, &s_ok, false);
+  if (threadIdx.x == 0) {
+    if (done) *reinterpret_cast<volatile uint64_t*>(ep_home) = ep + 1;
+    if (P.span) atomicMax(P.span + 1, static_cast<unsigned long long>(globaltimer()));
+  }
+}
+
+const void* pick_rs_tma(int dtype) {
+  switch (dtype) {
+    case LAGOM_F32: return reinterpret_cast<const void*>(&rs_tma_kernel<float>);
+    case LAGOM_BF16: return reinterpret_cast<const void*>(&rs_tma_kernel<__nv_bfloat16>);
+    case LAGOM_F16: return reinterpret_cast<const void*>(&rs_tma_kernel<__half>);
+    case LAGOM_I32: return reinterpret_cast<const void*>(&rs_tma_kernel<int32_t>);
+  }
+  return nullptr;
+}
+
+// the 192 KB dynamic smem ring of a TMA kernel, enabled once per kernel
+bool tma_smem_ok(const void* k) {
+  static const void* done[8] = {};
+  static bool ok[8] = {};
+  for (int i = 0; i < 8; ++i) {
+    if (done[i] == k) return ok[i];
+    if (!done[i]) {
+      done[i] = k;
+      ok[i] = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
+      return ok[i];
+    }
+  }
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
+}
+
 template <int KIND, int U, int MAXT, int MINB = 1>
 const void* pick_nvls_u(int dtype) {
   // the copy kinds (AG, A2A, one-hop AG) move bytes: one instantiation
@@ -616,7 +762,13 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
   if (!c->nvls_ready || a->algorithm != LAGOM_TREE || a->redop != LAGOM_SUM || c->virt) return 0;
   const int64_t e = ebytes(a->dtype), n = c->nranks;
   const bool co = c->opts.coresident != 0, hop = one_hop(c, a->num_channels);
-  const bool push_rs = hop && c->nvls_scratch && a->count * ebytes(a->dtype) <= c->nvls_scratch_slot;
+  // TMA data path for the one-hop kernels (one elected thread, 192 KB smem
+  // ring: an SM of its own) unless the config asks for the co-resident
+  // regime (NT <= 256)
+  const bool tma = c->opts.a2a_tma && !(co && a->num_threads <= 256);
+  const void* rs_tma = hop && tma && a->collective == LAGOM_REDUCE_SCATTER ? pick_rs_tma(a->dtype) : nullptr;
+  if (rs_tma && !tma_smem_ok(rs_tma)) rs_tma = nullptr;
+  const bool push_rs = hop && !rs_tma && c->nvls_scratch && a->count * ebytes(a->dtype) <= c->nvls_scratch_slot;
   int64_t in_b = 0, out_b = 0;
   const void* k = nullptr;
   switch (a->collective) {
@@ -624,30 +776,34 @@ int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const vo
     case LAGOM_ALL_GATHER:
       in_b = a->count * e;
       out_b = a->count * e * n;
+      if (hop && tma && tma_smem_ok(reinterpret_cast<const void*>(&ag_tma_kernel))) {
+        k = reinterpret_cast<const void*>(&ag_tma_kernel);
+        *smem_bytes = kA2aSmem;
+        break;
+      }
       k = hop ? pick_nvls<4>(a->dtype, a->num_threads, co) : pick_nvls<1>(a->dtype, a->num_threads, co);
       break;
     case LAGOM_REDUCE_SCATTER:
       in_b = a->count * e * n;
       out_b = a->count * e;
-      // one hop: push (partials into the owners' scratch, local reduce) when a
-      // scratch slot fits the block, else pull (peer loads; latency-bound)
+      // one hop: TMA pull when allowed; else push (partials into the owners'
+      // scratch, local reduce) when a scratch slot fits the block, else pull
+      // with vector loads (latency-bound)
+      if (rs_tma) {
+        k = rs_tma;
+        *smem_bytes = kA2aSmem;
+        break;
+      }
       k = !hop ? pick_nvls<2>(a->dtype, a->num_threads, co)
           : push_rs ? pick_nvls<6>(a->dtype, a->num_threads, co) : pick_nvls<5>(a->dtype, a->num_threads, co);
       break;
     case LAGOM_ALL_TO_ALL:
       if (!c->nvls_peers_ready) return 0;
       in_b = out_b = a->count * e * n;
-      // TMA bulk copies (one elected thread, 192 KB smem ring: an SM of its
-      // own) unless the config asks for the co-resident regime (NT <= 256)
-      if (c->opts.a2a_tma && !(co && a->num_threads <= 256)) {
-        static const bool smem_ok =
-            cudaFuncSetAttribute(reinterpret_cast<const void*>(&a2a_tma_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
-        if (smem_ok) {
-          k = reinterpret_cast<const void*>(&a2a_tma_kernel);
-          *smem_bytes = kA2aSmem;
-          break;
-        }
+      if (tma && tma_smem_ok(reinterpret_cast<const void*>(&a2a_tma_kernel))) {
+        k = reinterpret_cast<const void*>(&a2a_tma_kernel);
+        *smem_bytes = kA2aSmem;
+        break;
       }
       k = pick_nvls<3>(a->dtype, a->num_threads, co);
       break;

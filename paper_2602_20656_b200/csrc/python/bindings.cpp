@@ -365,7 +365,7 @@ PYBIND11_MODULE(_lagom_py, m) {
            py::arg("repeats") = 3, py::arg("warmup") = 1, py::arg("nccl") = true,
            py::arg("max_chunk_bytes") = 4 << 20, py::arg("max_channels") = 32, py::arg("e2e_in_bytes") = 0,
            py::arg("e2e_out_bytes") = 0, py::arg("sm_partition") = 1, py::arg("nvls") = false,
-           py::arg("coresident") = true, py::arg("one_hop") = 0, py::arg("a2a_tma") = true,
+           py::arg("coresident") = true, py::arg("one_hop") = 2, py::arg("a2a_tma") = true,
            py::arg("pm_interval_ns") = 20000)
       .def("workload", &PyEngine::workload, py::arg("gpu") = "")
       .def("run", &PyEngine::run)

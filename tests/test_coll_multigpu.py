@@ -51,14 +51,17 @@ def test_real_multigpu_parity(world, variant):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("a2a_tma", [1, 0])
 @pytest.mark.parametrize("world", [2, 4])
-def test_real_multigpu_parity_one_hop_allgather_reducescatter(world):
-    """TREE AllGather (peer stores) and ReduceScatter (peer loads, ring order;
-    LAGOM_ONE_HOP=1) instead of
-    the switch: bit-exact (the ReduceScatter combines in the ring order)."""
+def test_real_multigpu_parity_one_hop_allgather_reducescatter(world, a2a_tma):
+    """TREE AllGather and ReduceScatter over the peer mappings instead of the
+    switch (LAGOM_ONE_HOP=1): bit-exact (the ReduceScatter combines in the
+    ring order). a2a_tma = 1: TMA bulk stores (AG) and the TMA pull (RS) at
+    NT > 256, vector stores / the push into the owners' scratch at NT <= 256;
+    a2a_tma = 0: the vector kernels at every NT."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_ONE_HOP="1")
+    env = dict(os.environ, LAGOM_NVLS="1", LAGOM_ONE_HOP="1", LAGOM_A2A_TMA=str(a2a_tma))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_coll_check.py")]
@@ -72,7 +75,7 @@ def test_real_multigpu_parity_one_hop_allgather_reducescatter(world):
 def test_real_multigpu_parity_bench_sizes(world, one_hop):
     """The bench's own collectives at BASELINE sizes on real peers with NVLS
     on (TREE = in-switch AR/AG/RS, or with one_hop the peer-store AllGather
-    and the pipelined push ReduceScatter; one-hop A2A; RING = P2P rings),
+    and the TMA pull ReduceScatter at NT 512; one-hop A2A; RING = P2P rings),
     NC 8/16, NT 512, C 2 MiB: bit-exact, or within the fp64-exact-sum bound
     for the switch's fp32 sums."""
     if _gpus() < world:

@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--warm", type=int, default=2)
     ap.add_argument("--nccl", type=int, default=1)
     ap.add_argument("--batch", type=int, default=1, help="launches per timed group (per-launch time reported)")
+    ap.add_argument("--one-hop", type=int, default=0, help="lagom_comm_opts_t.one_hop (TREE AG/RS over peer mappings)")
     ap.add_argument("--lagom", type=int, default=1, help="0: NCCL rows only (e.g. under NCCL_ALGO=NVLS)")
     ap.add_argument("--out", default="")
     ap.add_argument("--nvls", type=int, default=0, help="buffers in an NVLS region (TREE runs in-switch)")
@@ -68,7 +69,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = C.Communicator.from_process_group(device=local, max_channels=64, use_tma=args.use_tma)
+    comm = C.Communicator.from_process_group(device=local, max_channels=64, use_tma=args.use_tma,
+                                             one_hop=args.one_hop)
     stream = torch.cuda.current_stream()
     s_ptr = stream.cuda_stream
     sizes = [parse_size(s) for s in args.sizes.split(",")]
@@ -124,7 +126,7 @@ def main():
                     ok = bool(torch.equal(y, y_ref))
                 else:
                     ok = bool(((y.float() - y_ref).abs() <= (2.0 ** -7) * world * mag + 1e-6).all())
-                rows.append(dict(impl="lagom", ok=ok, coll=cn, algo=int(algo), proto=int(proto), nc=int(nc), nt=int(nt),
+                rows.append(dict(impl="lagom", ok=ok, one_hop=args.one_hop, coll=cn, algo=int(algo), proto=int(proto), nc=int(nc), nt=int(nt),
                                  use_tma=args.use_tma, nvls=args.nvls, batch=args.batch,
                                  chunk=parse_size(ch), bytes=s_bytes, t_s=t, algbw=s_bytes / t / 1e9,
                                  busbw=s_bytes / t * fac / 1e9))

@@ -52,7 +52,8 @@ def main():
     ap.add_argument("--interval-ns", type=int, default=20000)
     ap.add_argument("--nvls", type=int, default=1)
     ap.add_argument("--sm-partition", type=int, default=1)
-    ap.add_argument("--one-hop", type=int, default=0, help="lagom_comm_opts_t.one_hop (bench.py default)")
+    ap.add_argument("--one-hop", type=int, default=0,
+                    help="lagom_comm_opts_t.one_hop (0: the setting of the committed round-2 counter profiles)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     rank, world, local = dist_env()
