@@ -385,7 +385,8 @@ def main():
         zsel = {st: [] for st in runs}
         order = list(runs)
         sel_rng = random.Random(args.order_seed + 1)
-        for i in range(6 if len(runs) > 1 else 0):  # random order per round: no start keeps a predecessor
+        # 12 rounds: with 6, identical-config spreads of a few % let the pick flip between sessions
+        for i in range(12 if len(runs) > 1 else 0):  # random order per round: no start keeps a predecessor
             perm = order[:]
             sel_rng.shuffle(perm)
             for st in perm:
@@ -478,7 +479,8 @@ def main():
     cfg_dom = full_cfgs[j_dom]
     t_ev = statistics.median(r["x_ev"][j_dom] for r in result["comm"])    # CUDA events, us
     t_span = statistics.median(r["x"][j_dom] for r in result["comm"])     # kernel's own span, us
-    one_hop_agrs = nvls_state["peer_mappings"] and (args.one_hop == 1 or (args.one_hop == 2 and world == 2))
+    one_hop_agrs = nvls_state["peer_mappings"] and (
+        args.one_hop == 1 or (args.one_hop == 2 and world == 2 and cfg_dom["num_channels"] >= 16))
     wb, sched = wire_bytes(op, world, cfg_dom, nvls_state["active"], nvls_state["peer_mappings"], one_hop_agrs)
     e = 2 if op["dtype"] in (1, 2) else 4
     S = op["count"] * e * (1 if op["collective"] == "ALL_REDUCE" else world)
@@ -504,8 +506,9 @@ def main():
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
             tr = json.load(f).get(f"{dag['name']}")
-        if isinstance(tr, dict) and tr.get("config") == roof["config"]:
-            roof["traffic"] = tr.get("bytes")
+        for t in (tr if isinstance(tr, list) else [tr]):  # one ncu capture per kernel config
+            if isinstance(t, dict) and t.get("config") == roof["config"]:
+                roof["traffic"] = t.get("bytes")
 
     gemm_flops = dags.flops(dag)
     cpu = None

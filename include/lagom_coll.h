@@ -77,7 +77,8 @@ typedef struct {
                               (AG: peer stores; RS: TMA pull of the peers' partials, or
                               pushes into the owners' scratch with vector stores, see
                               lagom_comm_nvls_scratch), 2 (default) one hop at nranks == 2
-                              (where the multicast echo doubles the switch's bytes)   */
+                              from 16 channels up (the multicast echo doubles the
+                              switch's bytes there; fewer SMs move less one hop)      */
   int a2a_tma;             /* 1 (default): the one-hop kernels (AllToAll, and with one_hop
                               the AllGather / ReduceScatter) move data with TMA bulk copies
                               (one elected thread, 192 KB smem ring: the CTA takes an SM)

@@ -748,12 +748,16 @@ int ebytes(int dtype) { return (dtype == LAGOM_BF16 || dtype == LAGOM_F16) ? 2 :
 // busbw from NC = 8 upward, while the one-hop schedules keep scaling with the
 // channels (AllGather on a 4xB200 pair, 1 GiB: NC 8: 216 vs 322; NC 15: 355
 // vs 278; NC 32: 569 vs 342 GB/s; profiles/round1_ag_one_hop_n2.jsonl).
-// one_hop = 2: one hop at n = 2 (every rank has the same n, so every rank
-// makes the same choice).
+// one_hop = 2: one hop at n = 2 from kOneHopMinChannels channels up, where
+// the per-SM rate of the peer copies (~55 GB/s with TMA) overtakes the
+// switch (n = 2, AG / RS 64 MiB, profiles/round2_onehop_scan_*_n2.jsonl:
+// NC 8: 161 / 202 us one hop vs 109 / 120 us switch; NC 16: 88 / 109 vs
+// 110 / 116; NC 24: 64 / 81 vs 116 / 121). Every rank has the same n and
+// launches the same config, so every rank makes the same choice.
+constexpr int kOneHopMinChannels = 16;
 bool one_hop(const lagom_comm* c, int nc) {
   const int mode = c->opts.one_hop;
-  (void)nc;
-  return c->nvls_peers_ready && (mode == 1 || (mode == 2 && c->nranks == 2));
+  return c->nvls_peers_ready && (mode == 1 || (mode == 2 && c->nranks == 2 && nc >= kOneHopMinChannels));
 }
 
 int lagom_nvls_prepare(const lagom_comm* c, const lagom_coll_args_t* a, const void* send, void* recv,

@@ -54,7 +54,9 @@ def dominant_roofline(d, n):
     cfg = d["tune"]["configs"][gd]
     t = statistics.median(r["x_ev"][j] for r in raw["comm"])
     nv = line["lagom"]["nvls"]
-    wb, _ = bench.wire_bytes(dag["comm_ops"][j], n, cfg, nv["active"], nv["peer_mappings"])
+    oh = line["lagom"].get("one_hop", 0)
+    hop = nv["peer_mappings"] and (oh == 1 or (oh == 2 and n == 2 and cfg["num_channels"] >= 16))
+    wb, _ = bench.wire_bytes(dag["comm_ops"][j], n, cfg, nv["active"], nv["peer_mappings"], hop)
     peak = line["roofline"]["peak"]
     return wb / (t * 1e-6) / 1e9 / peak, f"{cfg['algorithm']} NC{cfg['num_channels']}/NT{cfg['num_threads']}"
 
