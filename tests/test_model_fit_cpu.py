@@ -59,21 +59,31 @@ def test_predicted_overlap_time_all_rows(tmp_path, fit_cache, n, workload):
     assert (abs(got["rel_err"]["Z"]) <= 0.05) == ((n, workload) not in OUT_OF_BOUND)
 
 
-ROUND2 = [n for n in (4, 2) if os.path.exists(os.path.join(ROOT, "profiles", f"round2_model_n{n}.json"))]
+# Round 2's counter-backed models: (tag, N, model file, counter profiles, bench lines). "session3":
+# fitted to the counters and bench lines taken with the round-2 kernels before the barrier rework;
+# "final": the same fit over counters and bench lines of the final kernels.
+ROUND2 = []
+for _tag, _model, _counters, _bench in (
+        ("session3", "round2_model_session3_n{n}.json", "round2_counters_session3_n{n}_*.json",
+         "round2_session3_n{n}_*.json"),
+        ("final", "round2_model_n{n}.json", "round2_counters_n{n}_*.json", "round2_final_n{n}_*.json")):
+    for _n in (4, 2):
+        if os.path.exists(os.path.join(ROOT, "profiles", _model.format(n=_n))):
+            ROUND2.append((_tag, _n, _model.format(n=_n), _counters.format(n=_n), _bench.format(n=_n)))
 
 
-@pytest.mark.parametrize("n", ROUND2)
-def test_counter_model_rows_reproduce(tmp_path, n):
+@pytest.mark.parametrize("tag,n,model,counters,bench", ROUND2, ids=[f"{r[0]}-n{r[1]}" for r in ROUND2])
+def test_counter_model_rows_reproduce(tmp_path, tag, n, model, counters, bench):
     """Round 2's counter-backed model (tools/counter_fit.py) re-derived from
     the committed CUPTI counter profiles and bench lines with the committed
     global parameters: every config set's and every bench row's predicted Z
     is reproduced, so the errors DESIGN.md §7 states are the real ones —
     inside and outside the 5 % bound alike."""
     out = tmp_path / "model.json"
-    committed_path = os.path.join(ROOT, "profiles", f"round2_model_n{n}.json")
+    committed_path = os.path.join(ROOT, "profiles", model)
     subprocess.run([sys.executable, os.path.join(ROOT, "tools", "counter_fit.py"), "--n", str(n),
-                    "--profiles", os.path.join(ROOT, "profiles", f"round2_counters_n{n}_*.json"),
-                    "--bench", os.path.join(ROOT, "profiles", f"round2_session3_n{n}_*.json"),
+                    "--profiles", os.path.join(ROOT, "profiles", counters),
+                    "--bench", os.path.join(ROOT, "profiles", bench),
                     "--globals", committed_path, "--out", str(out)], cwd=ROOT, check=True, capture_output=True,
                    timeout=900)
     got, committed = json.load(open(out)), json.load(open(committed_path))

@@ -1,8 +1,9 @@
 """Prints DESIGN.md §6's result tables from the committed round-2 files:
 bench lines (profiles/round2_final_n{N}_{workload}.json, and the same
 session's repeat round2_final_rep2_n{N}_{workload}.json) and the
-counter-backed model (profiles/round2_model_n{N}.json, fitted to the
-counter profiles and the bench lines of session 3, round2_session3_*). No GPU.
+counter-backed models (profiles/round2_model_n{N}.json over the final
+kernels' counters and bench lines; round2_model_session3_n{N}.json over
+session 3's). No GPU.
 
   python tools/results_tables.py
 """
@@ -92,10 +93,10 @@ def bench_rows():
     return "\n".join(out)
 
 
-def model_rows():
+def model_rows(model="round2_model_n{n}.json"):
     out = ["| workload | N | picks | predicted Z (ms) | measured Z (ms) | error |", "|---|---|---|---|---|---|"]
     for n in (4, 2):
-        m = load(f"round2_model_n{n}.json")
+        m = load(model.format(n=n))
         if not m:
             continue
         for r in m["bench_rows"]:
@@ -106,10 +107,10 @@ def model_rows():
     return "\n".join(out)
 
 
-def model_set_summary():
+def model_set_summary(model="round2_model_n{n}.json"):
     out = ["| N | sets | median abs Z error | within 5 % | delta (dedicated / co-resident) |", "|---|---|---|---|---|"]
     for n in (4, 2):
-        m = load(f"round2_model_n{n}.json")
+        m = load(model.format(n=n))
         if not m:
             continue
         errs = sorted(abs(r["Z_err"]) for r in m["sets"])
@@ -122,7 +123,10 @@ def model_set_summary():
 
 if __name__ == "__main__":
     print(bench_rows())
-    print()
-    print(model_rows())
-    print()
-    print(model_set_summary())
+    for tag, model in (("final kernels", "round2_model_n{n}.json"),
+                       ("session 3 kernels", "round2_model_session3_n{n}.json")):
+        print()
+        print(f"model ({tag}):")
+        print(model_rows(model))
+        print()
+        print(model_set_summary(model))
