@@ -542,7 +542,8 @@ def main():
             "nccl_default": ms_nccl,
             "nccl_with_sm_partition": ms.get("nccl_partition"),
             "nccl_reserved_sms": result["nccl_reserve"] or None,
-            "ours_at_seed_no_partition" if args.sm_partition != 2 else "ours_at_seed": ms["seed"],
+            {0: "ours_at_seed_no_partition", 1: "ours_at_seed_auto_partition", 2: "ours_at_seed"}[args.sm_partition]:
+                ms["seed"],
             "ours_at_seed_partition_all": ms.get("seed_partition_all"),
             "ours_tuned": ms["lagom"],
             "tuned_equals_seed": same_cfg,

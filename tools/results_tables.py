@@ -68,7 +68,7 @@ def fmt(v, nd=2):
 
 def bench_rows():
     out = ["| workload (BASELINE config) | N | Lagom-tuned | NCCL-default | speedup | ours @ seed | "
-           "ours @ seed + SM partition | NCCL + SM partition | compute only | picks | compute slowdown "
+           "ours @ seed, partition always | NCCL + SM partition | compute only | picks | compute slowdown "
            "(Lagom / NCCL) | roofline frac (dominant group) | repeat: speedup, picks |",
            "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for n in (4, 2, 1):
