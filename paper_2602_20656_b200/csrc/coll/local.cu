@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "comm_internal.h"
@@ -34,7 +35,7 @@ struct LocalParams {
 
 // U 16-byte loads in flight per thread before the stores: ~32 KB per CTA in
 // every class (the per-SM copy rate is set by the bytes in flight).
-template <int MAXT, int U>
+template <int MAXT, int U, bool PF>
 __global__ void __launch_bounds__(MAXT, 3) local_copy_kernel(const __grid_constant__ LocalParams P) {
   const char* __restrict__ src = P.src;
   char* __restrict__ dst = P.dst;
@@ -54,7 +55,21 @@ __global__ void __launch_bounds__(MAXT, 3) local_copy_kernel(const __grid_consta
   const uint4* s = reinterpret_cast<const uint4*>(src + head) + tid;
   uint4* d = reinterpret_cast<uint4*>(dst + head) + tid;
   int64_t left = body - tid;  // units from this thread's position to the end
+  // The CTA's next batch is U chunks of nt units, `stride` apart: threads
+  // 0..U-1 each ask the TMA unit to prefetch one into L2 (no registers, no
+  // shared memory), so the batch's loads wait on L2 instead of HBM.
+  const int64_t chunk_bytes = nt * 16;
+  const int64_t cta_left = left + threadIdx.x;  // units from the CTA's first position to the end
+  const uint4* cta_src = s - threadIdx.x;
   for (; left > (U - 1) * stride; left -= U * stride) {
+    if (PF && threadIdx.x < U) {
+      const int64_t at = (U + static_cast<int64_t>(threadIdx.x)) * stride;  // chunk of the next batch
+      const int64_t done = (body - tid) - left;                             // units this CTA passed
+      if (cta_left - done - at >= nt)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cta_src + done + at),
+                     "r"(static_cast<uint32_t>(chunk_bytes))
+                     : "memory");
+    }
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u, s += stride) v[u] = __ldcs(s);
@@ -71,13 +86,23 @@ __global__ void __launch_bounds__(MAXT, 3) local_copy_kernel(const __grid_consta
 }
 
 // the thread-count class that holds NT (NT is a multiple of 64 in [64, 640])
+template <bool PF>
+const void* pick_pf(int nt) {
+  if (nt <= 64) return reinterpret_cast<const void*>(&local_copy_kernel<64, 32, PF>);
+  if (nt <= 128) return reinterpret_cast<const void*>(&local_copy_kernel<128, 16, PF>);
+  if (nt <= 256) return reinterpret_cast<const void*>(&local_copy_kernel<256, 7, PF>);
+  if (nt <= 384) return reinterpret_cast<const void*>(&local_copy_kernel<384, 4, PF>);
+  if (nt <= 512) return reinterpret_cast<const void*>(&local_copy_kernel<512, 3, PF>);
+  return reinterpret_cast<const void*>(&local_copy_kernel<640, 2, PF>);
+}
+// L2 prefetch of the next batch: on unless LAGOM_COPY_PREFETCH=0 (single
+// rank only, so a per-process choice needs no agreement)
 const void* pick(int nt) {
-  if (nt <= 64) return reinterpret_cast<const void*>(&local_copy_kernel<64, 32>);
-  if (nt <= 128) return reinterpret_cast<const void*>(&local_copy_kernel<128, 16>);
-  if (nt <= 256) return reinterpret_cast<const void*>(&local_copy_kernel<256, 7>);
-  if (nt <= 384) return reinterpret_cast<const void*>(&local_copy_kernel<384, 4>);
-  if (nt <= 512) return reinterpret_cast<const void*>(&local_copy_kernel<512, 3>);
-  return reinterpret_cast<const void*>(&local_copy_kernel<640, 2>);
+  static const bool pf = [] {
+    const char* e = std::getenv("LAGOM_COPY_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
+  return pf ? pick_pf<true>(nt) : pick_pf<false>(nt);
 }
 
 }  // namespace
