@@ -98,6 +98,13 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint
                "r"(bytes)
                : "memory");
 }
+// Asks the TMA unit to pull [p, p + bytes) into L2 (16 B aligned, 16 B
+// multiple): no registers or shared memory held, so register-capped kernels
+// get their next batch's loads served from L2 instead of HBM.
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  if (bytes > 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(static_cast<uint32_t>(bytes)) : "memory");
+}
 __device__ __forceinline__ void mbar_init_count(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }

@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
       char* out = P.peer_recv[p] + static_cast<int64_t>(r) * units * 16;
       int64_t u0 = lo + threadIdx.x;
       for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+        if (threadIdx.x == 0 && u0 + nt * U < hi)  // the CTA's next batch into L2
+          lagom_dev::prefetch_l2(in + (u0 + nt * U) * 16, lagom_dev::lmin(nt * U, hi - u0 - nt * U) * 16);
         const char* src = in + u0 * 16;
         char* dst = out + u0 * 16;
         uint4 v[U];
@@ -259,6 +261,8 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
     const int64_t at = static_cast<int64_t>(r) * units * 16;
     int64_t u0 = lo + threadIdx.x;
     for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+      if (threadIdx.x == 0 && u0 + nt * U < hi)  // the CTA's next batch into L2
+        lagom_dev::prefetch_l2(in + (u0 + nt * U) * 16, lagom_dev::lmin(nt * U, hi - u0 - nt * U) * 16);
       uint4 v[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) v[j] = *reinterpret_cast<const uint4*>(in + (u0 + j * nt) * 16);
@@ -310,6 +314,8 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
         src += threadIdx.x;
         dst += threadIdx.x;
         for (; left > (U - 1) * nt; left -= U * nt) {
+          if (threadIdx.x == 0 && left > U * nt)  // the CTA's next batch into L2
+            lagom_dev::prefetch_l2(src + U * nt, lagom_dev::lmin(U * nt, left - U * nt) * 16);
           uint4 v[U];
 #pragma unroll
           for (int j = 0; j < U; ++j) v[j] = src[j * nt];
@@ -344,6 +350,10 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
       const int64_t a = lo + i * pu, b = lagom_dev::lmin(hi, a + pu);
       uint4* out = reinterpret_cast<uint4*>(P.recv_uc);
       for (int64_t u = a + threadIdx.x; u < b; u += nt * U) {
+        if (threadIdx.x < n && u - threadIdx.x + nt * U < b) {  // every part's next batch into L2
+          const int64_t nb = u - threadIdx.x + nt * U;
+          lagom_dev::prefetch_l2(part((r + 1 + threadIdx.x) % n) + nb, lagom_dev::lmin(nt * U, b - nb) * 16);
+        }
         uint4 acc[U];
 #pragma unroll
         for (int j = 0; j < U; ++j)
@@ -436,6 +446,8 @@ __global__ void __launch_bounds__(MAXT, MINB) nvls_kernel(const __grid_constant_
   };
   int64_t u0 = lo + threadIdx.x;
   for (; u0 + (U - 1) * nt < hi; u0 += nt * U) {
+    if (KIND == 1 && threadIdx.x == 0 && u0 + nt * U < hi)  // AG reads locally: next batch into L2
+      lagom_dev::prefetch_l2(in + (u0 + nt * U) * 16, lagom_dev::lmin(nt * U, hi - u0 - nt * U) * 16);
     const char* src = in + u0 * 16;
     char* dst = out + u0 * 16;
     uint4 v[U];
