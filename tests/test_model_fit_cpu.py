@@ -61,12 +61,13 @@ def test_predicted_overlap_time_all_rows(tmp_path, fit_cache, n, workload):
 
 # Round 2's counter-backed models: (tag, N, model file, counter profiles, bench lines). "session3":
 # fitted to the counters and bench lines taken with the round-2 kernels before the barrier rework;
-# "final": the same fit over counters and bench lines of the final kernels.
+# "final": the same fit over the counters and bench lines (session B) of the final kernels before the
+# L2 prefetch of the local-read kernels.
 ROUND2 = []
 for _tag, _model, _counters, _bench in (
         ("session3", "round2_model_session3_n{n}.json", "round2_counters_session3_n{n}_*.json",
          "round2_session3_n{n}_*.json"),
-        ("final", "round2_model_n{n}.json", "round2_counters_n{n}_*.json", "round2_final_n{n}_*.json")):
+        ("final", "round2_model_n{n}.json", "round2_counters_n{n}_*.json", "round2_final_sessB_n{n}_*.json")):
     for _n in (4, 2):
         if os.path.exists(os.path.join(ROOT, "profiles", _model.format(n=_n))):
             ROUND2.append((_tag, _n, _model.format(n=_n), _counters.format(n=_n), _bench.format(n=_n)))

@@ -123,7 +123,7 @@ def model_set_summary(model="round2_model_n{n}.json"):
 
 if __name__ == "__main__":
     print(bench_rows())
-    for tag, model in (("final kernels", "round2_model_n{n}.json"),
+    for tag, model in (("final kernels before the L2 prefetch, session B bench lines", "round2_model_n{n}.json"),
                        ("session 3 kernels", "round2_model_session3_n{n}.json")):
         print()
         print(f"model ({tag}):")
