@@ -67,7 +67,10 @@ ROUND2 = []
 for _tag, _model, _counters, _bench in (
         ("session3", "round2_model_session3_n{n}.json", "round2_counters_session3_n{n}_*.json",
          "round2_session3_n{n}_*.json"),
-        ("final", "round2_model_n{n}.json", "round2_counters_n{n}_*.json", "round2_final_sessB_n{n}_*.json")):
+        ("final", "round2_model_n{n}.json", "round2_counters_n{n}_*.json", "round2_final_sessB_n{n}_*.json"),
+        # the same with the two-rank one-hop schedules in their own subspace (counter_fit --one-hop-min-nc)
+        ("final-onehop", "round2_model_onehop_n{n}.json", "round2_counters_n{n}_*.json",
+         "round2_final_sessB_n{n}_*.json")):
     for _n in (4, 2):
         if os.path.exists(os.path.join(ROOT, "profiles", _model.format(n=_n))):
             ROUND2.append((_tag, _n, _model.format(n=_n), _counters.format(n=_n), _bench.format(n=_n)))

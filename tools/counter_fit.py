@@ -54,8 +54,26 @@ def hbm_peak():
     return (json.load(open(p))["hbm_gbs"] if os.path.exists(p) else 6540.8) * 1e3  # bytes/us
 
 
-def key_of(cfg):
+# At two ranks the product runs TREE AllGather / ReduceScatter one hop from
+# ONE_HOP_MIN_NC channels up (lagom_comm_opts_t.one_hop = 2), and through the
+# switch below: two schedules inside one reference subspace, which one
+# comm_time curve cannot fit. With --one-hop-min-nc the one-hop configs get
+# their own subspace key (transport SHM: the reference's Transport enum, used
+# here as the "peer mappings, not the switch" label) in the fitted params and
+# in the configs handed to simulate(). None: one key per (algorithm, protocol).
+ONE_HOP_MIN_NC = None
+
+
+def key_of(cfg, coll=None, n=None):
+    if (ONE_HOP_MIN_NC and n == 2 and cfg["algorithm"] == "TREE" and coll in ("ALL_GATHER", "REDUCE_SCATTER")
+            and cfg["num_channels"] >= ONE_HOP_MIN_NC):
+        return f"{cfg['algorithm']}/{cfg['protocol']}/SHM"
     return f"{cfg['algorithm']}/{cfg['protocol']}/P2P"
+
+
+def with_key(cfg, coll, n):
+    """cfg as simulate() must see it: transport per key_of."""
+    return dict(cfg, transport=key_of(cfg, coll, n).split("/")[2])
 
 
 def coresident(cfg, nvls):
@@ -112,14 +130,16 @@ def fit_params(wls, extra=()):
         for st in wl.prof["sets"].values():
             cfg = st["config"]
             for j, co in enumerate(st["comm_ops"]):
-                by_key.setdefault(key_of(cfg), {}).setdefault(wl.dag["comm_ops"][j]["collective"], []).append(
+                coll = wl.dag["comm_ops"][j]["collective"]
+                by_key.setdefault(key_of(cfg, coll, wl.n), {}).setdefault(coll, []).append(
                     (cfg["num_channels"], cfg["num_threads"], cfg["chunk_size"], wl.sizes[j], co["x_us"]))
     params, report, links = {}, {}, {}
     factors = {"ALL_REDUCE": 2.0}
     main_key = max(by_key, key=lambda k: sum(len(v) for v in by_key[k].values()))
-    for key, colls in by_key.items():
+    # the main subspace first: its collective factors scale the other subspaces' base points
+    for key, colls in sorted(by_key.items(), key=lambda kv: kv[0] != main_key):
         base = "ALL_REDUCE" if "ALL_REDUCE" in colls else max(colls, key=lambda c: len(colls[c]))
-        bf = 2.0 if base == "ALL_REDUCE" else 1.0
+        bf = 2.0 if base == "ALL_REDUCE" else (factors.get(base, 1.0) if key != main_key else 1.0)
         co, lk, rep = fit([(nc, nt, c, m * bf, x) for nc, nt, c, m, x in colls[base]])
         params[key], links[key] = co, lk
         report[key] = dict(rep, link_bw=lk, base_collective=base)
@@ -142,7 +162,7 @@ def fit_params(wls, extra=()):
         for wl in wls:
             for st in wl.prof["sets"].values():
                 cfg = st["config"]
-                if key_of(cfg) == key:
+                if key_of(cfg, wl.dag["comm_ops"][0]["collective"], wl.n) == key:
                     xs = sum(c["x_us"] for c in st["comm_ops"])
                     vpts.append((cfg["num_channels"], cfg["chunk_size"],
                                  sum(c["dram_bytes"] for c in st["comm_ops"]) / xs))
@@ -168,7 +188,8 @@ def fit_params(wls, extra=()):
 def predict(wl, cfgs, params, links, g, nvls, y_iso=None):
     from paper_2602_20656_b200 import _lagom_py as L
     co = all(coresident(c, nvls) for c in cfgs)
-    key = key_of(cfgs[0])
+    cfgs = [with_key(c, op["collective"], wl.n) for c, op in zip(cfgs, wl.dag["comm_ops"])]
+    key = "/".join((cfgs[0]["algorithm"], cfgs[0]["protocol"], cfgs[0]["transport"]))
     bw = g["B_co"] if co else g["B_ded"]
     gpu = {"num_sms": LAMBDA, "link_bw": links.get(key, next(iter(links.values()))), "comm_bw_cap_fraction": 0.6,
            "compute_on_comm_slowdown": g["delta_co"] if co else g["delta_ded"]}
@@ -185,7 +206,14 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--globals", default="", help="take the four global parameters from this model file "
                     "instead of the grid search (re-derives its rows; tests/test_model_fit_cpu.py)")
+    ap.add_argument("--one-hop-min-nc", type=int, default=0,
+                    help="two-rank TREE AG/RS at >= this NC get their own subspace (the product's one_hop = 2 "
+                         "threshold, 16; 0 = off). Taken from --globals' file when it records one")
     a = ap.parse_args()
+    global ONE_HOP_MIN_NC
+    ONE_HOP_MIN_NC = a.one_hop_min_nc or None
+    if a.globals:
+        ONE_HOP_MIN_NC = json.load(open(a.globals)).get("one_hop_min_nc") or ONE_HOP_MIN_NC
     profs = [json.load(open(p)) for f in a.profiles for p in sorted(glob.glob(f))]
     wls = [Workload(p) for p in profs if p["n"] == a.n]
     benches = []
@@ -205,7 +233,8 @@ def main():
         cfgs = [b["tune"]["configs"][gi] for gi in _groups(wl.dag)]
         xs = np.median([r["x"] for r in b["raw"]["comm"]], axis=0)
         for j, cfg in enumerate(cfgs):
-            extra.append((key_of(cfg), wl.dag["comm_ops"][j]["collective"], cfg["num_channels"], cfg["num_threads"],
+            extra.append((key_of(cfg, wl.dag["comm_ops"][j]["collective"], a.n), wl.dag["comm_ops"][j]["collective"],
+                          cfg["num_channels"], cfg["num_threads"],
                           cfg["chunk_size"], wl.sizes[j], float(xs[j])))
     params, report, links = fit_params(wls, extra)
     B = hbm_peak()
@@ -256,7 +285,8 @@ def main():
         bench_rows.append({"workload": wname, "n": a.n, "picks": sorted(set(line["lagom"]["tune"]["picks"])),
                            "coresident": co, "Z_pred": sim["Z"], "Z_meas": meas, "Z_err": (sim["Z"] - meas) / meas,
                            "Y_pred": sim["Y"], "Y_meas": line["compute"]["overlapped_ms"] * 1e3})
-    res = {"n": a.n, "global": g, "fit_score_median_abs_Z_err": best[0], "params": params, "fit_report": report,
+    res = {"n": a.n, "one_hop_min_nc": ONE_HOP_MIN_NC, "global": g, "fit_score_median_abs_Z_err": best[0],
+           "params": params, "fit_report": report,
            "sets": rows, "bench_rows": bench_rows,
            "note": "sets: the profile's own overlapped replays (every comm op at one config); bench_rows: bench.py's "
                    "Lagom arm at the tuned picks, measured in a separate run"}
