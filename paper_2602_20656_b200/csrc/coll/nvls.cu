@@ -24,6 +24,9 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "comm_internal.h"
 #include "device.cuh"
@@ -687,18 +690,16 @@ const void* pick_rs_tma(int dtype) {
 }
 
 // the 192 KB dynamic smem ring of a TMA kernel, enabled once per kernel
+// (communicators may launch from several host threads)
 bool tma_smem_ok(const void* k) {
-  static const void* done[8] = {};
-  static bool ok[8] = {};
-  for (int i = 0; i < 8; ++i) {
-    if (done[i] == k) return ok[i];
-    if (!done[i]) {
-      done[i] = k;
-      ok[i] = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
-      return ok[i];
-    }
-  }
-  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, bool>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == k) return d.second;
+  const bool ok = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kA2aSmem) == cudaSuccess;
+  done.emplace_back(k, ok);
+  return ok;
 }
 
 template <int KIND, int U, int MAXT, int MINB = 1>
