@@ -62,7 +62,13 @@ __global__ void __launch_bounds__(MAXT, 3) local_copy_kernel(const __grid_consta
   const int64_t cta_left = left + threadIdx.x;  // units from the CTA's first position to the end
   const uint4* cta_src = s - threadIdx.x;
   for (; left > (U - 1) * stride; left -= U * stride) {
-    if (PF && threadIdx.x < U) {
+    if (PF && gridDim.x == 1) {
+      // one CTA: the next batch is one contiguous run of U chunks, one prefetch
+      if (threadIdx.x == 0 && left > U * stride)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s + U * stride),
+                     "r"(static_cast<uint32_t>(lagom_dev::lmin(U * stride, left - U * stride) * 16))
+                     : "memory");
+    } else if (PF && threadIdx.x < U) {
       const int64_t at = (U + static_cast<int64_t>(threadIdx.x)) * stride;  // chunk of the next batch
       const int64_t done = (body - tid) - left;                             // units this CTA passed
       if (cta_left - done - at >= nt)
